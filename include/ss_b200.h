@@ -1,0 +1,163 @@
+/*
+ * ss_b200.h -- C ABI of the B200-native steady-state solver for the driven,
+ * damped optomechanical Liouvillian of arXiv:1411.4356.
+ *
+ * The operation the library performs is the paper's statement of the problem:
+ *   find rho_ss with  L~ vec(rho_ss) = (w, 0, ..., 0)^T            Eq. (5)
+ *   L[rho] = -i[H,rho] + kappa D[a] + Gamma_m(1+n_th) D[b] + Gamma_m n_th D[b^+]
+ *                                                                   Eq. (3)
+ *   H = -Delta a^+a + omega_m b^+b + g0 (b+b^+) a^+a + E (a+a^+)    Eq. (1)
+ * vec() column stacking, a = a (x) I_b, b = I_a (x) b,
+ * solved by GMRES(m) on the reverse-Cuthill-McKee permuted L~
+ * (sec. III) with an incomplete-LU dual-threshold preconditioner
+ * (sec. II) applied from the left (Eq. (8)).
+ *
+ * Conventions for every entry point
+ *  - complex128 values are interleaved (re, im) pairs of IEEE doubles, 16-byte
+ *    aligned; "a complex vector of length n" is 2n doubles.
+ *  - index arrays are int64 on the host side of the ABI (int32 column indices
+ *    are used internally on the device; n and row lengths are < 2^31).
+ *  - "device pointer" = a CUDA global-memory address on the handle's device,
+ *    owned by the caller (e.g. a torch tensor's data_ptr()); "host pointer" =
+ *    ordinary (optionally pinned) host memory owned by the caller.
+ *  - the library owns every buffer it allocates inside a handle; they are
+ *    released by ss_destroy.  All device work runs on the CUDA stream given to
+ *    ss_build (NULL = legacy default stream); every call returns only after
+ *    its work on that stream has completed unless stated otherwise.
+ *  - return value: SS_OK (0) on success, otherwise one of the SS_ERR_* codes;
+ *    ss_last_error() then returns a NUL-terminated, thread-local message.
+ *    On error the handle stays valid (it may need ss_setup again).
+ *  - there is NO CPU fallback: without a CUDA device every call that computes
+ *    returns SS_ERR_CUDA.
+ */
+#ifndef SS_B200_H
+#define SS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SS_OK 0
+#define SS_ERR_ARG 1        /* invalid argument (sizes, NULL, ranges)                */
+#define SS_ERR_CUDA 2       /* CUDA runtime error / no device                        */
+#define SS_ERR_OOM 3        /* device or host allocation failed                       */
+#define SS_ERR_BREAKDOWN 4  /* ILUT zero pivot that cannot be repaired (drop_tol = 0)  */
+#define SS_ERR_STATE 5      /* call out of order (e.g. ss_solve before ss_setup)      */
+
+/* Physical parameters, Eq. (1) and Eq. (3); all rates in units of omega_m. */
+typedef struct ss_params {
+    int32_t N_c;        /* cavity Fock cut-off   (>= 1)                                */
+    int32_t N_m;        /* mechanical Fock cut-off (>= 1); Hilbert dim N = N_c N_m     */
+    double omega_m;     /* mechanical frequency                                        */
+    double Delta;       /* pump-cavity detuning  (H term -Delta a^+a)                  */
+    double kappa;       /* cavity decay rate  (>= 0)                                   */
+    double g0;          /* vacuum optomechanical coupling                              */
+    double E;           /* pump amplitude                                              */
+    double Gamma_m;     /* mechanical damping (>= 0)                                   */
+    double n_th;        /* bath occupation (>= 0)                                      */
+    double w;           /* trace weight of Eq. (5); NaN -> mean of diag(L) */
+} ss_params;
+
+typedef struct ss_problem ss_problem;   /* opaque handle: one Liouvillian on one GPU */
+
+typedef struct ss_build_info {
+    int64_t hilbert_dim;   /* N = N_c N_m                                  */
+    int64_t n;             /* Liouvillian dimension N^2                    */
+    int64_t nnz;           /* stored entries of L~ (exact zeros pruned)    */
+    double w_re, w_im;     /* the trace weight used                        */
+    double build_ms;       /* device time of the assembly                  */
+} ss_build_info;
+
+typedef struct ss_setup_info {
+    int64_t nnz_L;          /* strict lower entries of the ILU factor (unit diag implicit) */
+    int64_t nnz_U;          /* upper entries incl. the diagonal                             */
+    double fill;            /* (nnz_L + nnz_U) / nnz(L~)  -- Fig. 3 "fill-factor"            */
+    int64_t bandwidth_nat;  /* B(L~), sec. II                                                */
+    int64_t bandwidth_rcm;  /* B(L~_RCM)                                                      */
+    int64_t levels_L;       /* dependency levels of the forward / backward substitutions    */
+    int64_t levels_U;
+    int32_t pivots_repaired;/* zero pivots replaced by tau_i (reading R6)                     */
+    int32_t threads;        /* host threads used by the factorisation                        */
+    double rcm_ms, ilut_ms, upload_ms;
+} ss_setup_info;
+
+typedef struct ss_solve_info {
+    int32_t iterations;     /* Arnoldi steps = applications of M^{-1} L~                 */
+    int32_t cycles;         /* GMRES restarts performed                                  */
+    int32_t converged;      /* 1 iff rel_residual <= tol                                 */
+    int32_t pad;
+    double rel_residual;    /* true ||b - L~ x||_2 / ||b||_2 at exit (x before rescaling) */
+    double trace_re, trace_im; /* Tr(rho) before normalisation                            */
+    double solve_ms;        /* device time of the whole solve                             */
+} ss_solve_info;
+
+/* ---------------- the four calls of the method ---------------- */
+
+/* Assemble L~ of Eq. (5) (natural order, CSR, complex128) on the current CUDA device,
+ * on stream `cuda_stream` (a cudaStream_t, may be NULL).  *out receives a new handle. */
+int ss_build(const ss_params* p, void* cuda_stream, ss_problem** out, ss_build_info* info);
+
+/* One-time setup: RCM ordering of pattern(L~ + L~^T) (sec. III), the symmetric
+ * permutation L~_RCM, the ILUT(drop_tol, fill_factor) factors (sec. II; rules
+ * R4-R7 of DESIGN.md), their level schedules and the device layout of the hot
+ * path.  n_threads <= 0 -> all host cores.  May be called again with other
+ * drop_tol / fill_factor. */
+int ss_setup(ss_problem* h, double drop_tol, double fill_factor, int32_t n_threads,
+             ss_setup_info* info);
+
+/* Solve Eq. (5) by left-preconditioned GMRES(restart) (Eq. (8)) from
+ * x0 = 0 to the true relative residual tol, at most max_iter Arnoldi steps.  The
+ * solution is normalised to Tr rho = 1 (reading R11) and kept on the device. */
+int ss_solve(ss_problem* h, int32_t restart, double tol, int32_t max_iter, ss_solve_info* info);
+
+/* Observables of the last solution: <a^+a> = Tr(rho a^+a), <b^+b> = Tr(rho b^+b). */
+int ss_expect(ss_problem* h, double* n_cavity, double* n_mech);
+
+/* Copy the last solution rho (N x N complex128, column-major == vec(rho) of Eq. (4))
+ * to dst (N*N*16 bytes), a device pointer if dst_is_device else a host pointer. */
+int ss_get_rho(ss_problem* h, void* dst, int32_t dst_is_device);
+
+/* End-to-end variant for callers holding HOST buffers: copies rhs (natural order,
+ * length n, host) to the device, runs the same GMRES, copies the raw solution x
+ * (natural order, length n, not normalised) back to x_host.  rhs_host == NULL uses
+ * the Eq. (5) right-hand side.  The copies are part of the call. */
+int ss_solve_host(ss_problem* h, const double* rhs_host, double* x_host, int32_t restart,
+                  double tol, int32_t max_iter, ss_solve_info* info);
+
+void ss_destroy(ss_problem* h);
+const char* ss_last_error(void);
+
+/* ---------------- kernel-level entry points (parity tests, benchmark) ---------------- */
+
+/* Dimensions: n, nnz(L~); after ss_setup also nnz_L, nnz_U (else -1). */
+int ss_sizes(const ss_problem* h, int64_t* n, int64_t* nnz, int64_t* nnz_L, int64_t* nnz_U);
+
+/* Copy L~ (which = 0: natural order; 1: RCM order, needs ss_setup) to host CSR arrays:
+ * rowptr[n+1], colidx[nnz] (int64), vals[2*nnz] (complex128). Columns ascending. */
+int ss_export_matrix(const ss_problem* h, int32_t which, int64_t* rowptr, int64_t* colidx,
+                     double* vals);
+
+/* Copy the RCM permutation perm[n] (new -> old: L~_RCM = L~[perm][:, perm]). */
+int ss_export_perm(const ss_problem* h, int64_t* perm);
+
+/* Copy an ILU factor to host CSR: which = 0: strict lower L (unit diagonal implicit),
+ * rowptr[n+1], colidx[nnz_L], vals[2 nnz_L]; which = 1: U with its diagonal FIRST in
+ * every row then strict upper columns ascending, rowptr[n+1], colidx[nnz_U], vals[2 nnz_U]. */
+int ss_export_factors(const ss_problem* h, int32_t which, int64_t* rowptr, int64_t* colidx,
+                      double* vals);
+
+/* y = L~_RCM x  (device pointers, complex128 length n).                           */
+int ss_spmv(ss_problem* h, const void* x_dev, void* y_dev);
+/* y = L^{-1} x (which = 0), y = U^{-1} x (which = 1), y = U^{-1} L^{-1} x (which = 2);
+ * device pointers, length n, x and y may not alias.                                */
+int ss_precond(ss_problem* h, int32_t which, const void* x_dev, void* y_dev);
+
+/* Number of CUDA kernels this library has launched since load (gpu_launches evidence). */
+int64_t ss_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SS_B200_H */

@@ -1,0 +1,91 @@
+"""Oracle: dual-threshold incomplete LU (sec. II) -- Python face of ilut.c.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+PAPER.md:94: "incomplete LU factorization with dual-threshold ... a drop
+tolerance d and allowed fill-in p are specified such that all fill-in smaller
+than d times the infinity-norm of a row are dropped, and at most only
+p NNZ(L~) fill-in elements are allowed ... In the limit where d=0, the iLU
+preconditioner returns the complete LU factorization".
+The arithmetic is in oracle/ilut.c (rules R4-R7 of DESIGN.md, restated there).
+
+Also: condest(), the paper's estimate ||M e||_inf of the approximate inverse,
+PAPER.md:126 -- read (R8) as ||(LU)^{-1} e||_inf, e = (1,...,1)^T.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _clib
+
+
+@dataclass
+class IluFactors:
+    n: int
+    Lp: np.ndarray   # unit lower triangular, strict part only, CSR (cols ascending)
+    Lj: np.ndarray
+    Lx: np.ndarray
+    Up: np.ndarray   # upper triangular, diagonal FIRST in each row, then cols ascending
+    Uj: np.ndarray
+    Ux: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return len(self.Lj) + len(self.Uj)
+
+    def L(self) -> sp.csr_matrix:
+        """Strictly lower part as a canonical CSR (unit diagonal not stored)."""
+        return sp.csr_matrix((self.Lx, self.Lj, self.Lp), shape=(self.n, self.n))
+
+    def U(self) -> sp.csr_matrix:
+        M = sp.csr_matrix((self.Ux, self.Uj, self.Up), shape=(self.n, self.n))
+        M = M.copy()
+        M.sort_indices()
+        return M
+
+    def diag(self) -> np.ndarray:
+        return self.Ux[self.Up[:-1]]
+
+
+def ilut(A, drop_tol: float, fill_factor: float) -> IluFactors:
+    A = sp.csr_matrix(A)
+    A.sort_indices()
+    n = A.shape[0]
+    rp = np.ascontiguousarray(A.indptr, dtype=np.int64)
+    ci = np.ascontiguousarray(A.indices, dtype=np.int64)
+    v = np.ascontiguousarray(A.data, dtype=np.complex128)
+    P64 = ctypes.POINTER(ctypes.c_int64)
+    PD = ctypes.POINTER(ctypes.c_double)
+    Lp, Lj, Up, Uj = P64(), P64(), P64(), P64()
+    Lx, Ux = PD(), PD()
+    Ln, Un = ctypes.c_int64(), ctypes.c_int64()
+    lib = _clib.lib()
+    rc = lib.oracle_ilut(n, rp.ctypes.data_as(P64), ci.ctypes.data_as(P64), v.view(np.float64).ctypes.data_as(PD),
+                         float(drop_tol), float(fill_factor),
+                         ctypes.byref(Lp), ctypes.byref(Lj), ctypes.byref(Lx), ctypes.byref(Ln),
+                         ctypes.byref(Up), ctypes.byref(Uj), ctypes.byref(Ux), ctypes.byref(Un))
+    if rc != 0:
+        raise RuntimeError(f"oracle ILUT failed (rc={rc}): zero pivot at row {-rc - 1}" if rc > -2000000000
+                           else "oracle ILUT: out of memory")
+
+    def take(pp, jj, xx, nn):
+        p = np.ctypeslib.as_array(pp, (n + 1,)).copy()
+        j = np.ctypeslib.as_array(jj, (nn,)).copy() if nn else np.zeros(0, np.int64)
+        x = np.ctypeslib.as_array(xx, (2 * nn,)).copy().view(np.complex128) if nn else np.zeros(0, np.complex128)
+        for q in (pp, jj, xx):
+            lib.oracle_free(ctypes.cast(q, ctypes.c_void_p))
+        return p, j, x
+
+    lp, lj, lx = take(Lp, Lj, Lx, Ln.value)
+    up, uj, ux = take(Up, Uj, Ux, Un.value)
+    return IluFactors(n, lp, lj, lx, up, uj, ux)
+
+
+def condest(F: IluFactors) -> float:
+    """||(LU)^{-1} e||_inf, PAPER.md:126 (reading R8)."""
+    from .trisolve import apply_preconditioner
+    return float(np.abs(apply_preconditioner(F, np.ones(F.n, dtype=np.complex128))).max())

@@ -1,0 +1,52 @@
+"""Oracle: applying the ILU preconditioner, M^{-1} v = U^{-1} L^{-1} v (Eq. (8)).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+PAPER.md:84-87 (Eq. (8)): the preconditioned system M^{-1} L~ rho = M^{-1} b
+with M = L U from the incomplete factorisation.  Applying M^{-1}
+is a forward substitution with the unit lower factor followed by a backward
+substitution with the upper factor.  ``forward``/``backward`` are the textbook
+loops (small inputs); ``apply_preconditioner`` uses scipy's
+spsolve_triangular (a library primitive) for large ones.
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.sparse as sp
+import scipy.sparse.linalg as sla
+
+
+def forward(F, b: np.ndarray) -> np.ndarray:
+    """y_i = b_i - sum_{j<i} l_ij y_j   (unit diagonal)."""
+    y = np.array(b, dtype=np.complex128)
+    for i in range(F.n):
+        s = y[i]
+        for q in range(F.Lp[i], F.Lp[i + 1]):
+            s -= F.Lx[q] * y[F.Lj[q]]
+        y[i] = s
+    return y
+
+
+def backward(F, y: np.ndarray) -> np.ndarray:
+    """x_i = (y_i - sum_{j>i} u_ij x_j) / u_ii."""
+    x = np.array(y, dtype=np.complex128)
+    for i in range(F.n - 1, -1, -1):
+        q0 = F.Up[i]
+        s = x[i]
+        for q in range(q0 + 1, F.Up[i + 1]):
+            s -= F.Ux[q] * x[F.Uj[q]]
+        x[i] = s / F.Ux[q0]
+    return x
+
+
+def lower_unit_matrix(F) -> sp.csr_matrix:
+    return sp.csr_matrix(F.L() + sp.identity(F.n, dtype=np.complex128, format="csr"))
+
+
+def apply_preconditioner(F, v: np.ndarray, small_loops: bool = False) -> np.ndarray:
+    if small_loops:
+        return backward(F, forward(F, v))
+    Lm = lower_unit_matrix(F)
+    Um = F.U()
+    y = sla.spsolve_triangular(Lm, np.asarray(v, dtype=np.complex128), lower=True, unit_diagonal=True)
+    return sla.spsolve_triangular(Um, y, lower=False)

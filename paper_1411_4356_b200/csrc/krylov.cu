@@ -1,0 +1,423 @@
+// krylov.cu -- restarted, left-preconditioned GMRES(m) on the device.
+//
+// PAPER.md:126 (sec. IV): "we perform preconditioned iterations using the Restarted
+// Generalized Minimum Residual (GMRES) solver"; Eq. (8): left
+// preconditioning M^{-1} L~ x = M^{-1} b.  Stopping rule R9: the true
+// residual ||b - A x|| / ||b|| <= tol, checked at the start of every cycle; inside a
+// cycle the Givens residual estimate |g_{j+1}| is driven below
+// beta * tol * ||b|| / ||r_c||.
+//
+// Orthogonalisation is classical Gram-Schmidt with one re-orthogonalisation (CGS2),
+// organised as three streaming passes over the basis V (reading (j+1) n complex
+// each): A: h1 = V^H w;  B: w <- w - V h1 and h2 = V^H w;  C: w <- w - V h2 and
+// ||w||^2.  Each pass is one kernel over 32-element tiles: the (j+1) x 32 tile of V
+// is staged in shared memory, the update uses it, the dot products re-use it, so V
+// is read from HBM once per pass.  Reductions are two-stage with a fixed order
+// (block partials, then one block per output) -- deterministic, no atomics.
+// The 1-thread Hessenberg/Givens step runs on the device; the host only reads one
+// status word per Arnoldi step to decide whether to stop.
+#include <cstdio>
+
+#include "problem.h"
+
+namespace ssb {
+
+namespace {
+
+constexpr int kTile = 32;       // elements per tile
+constexpr int kCgsThreads = 256;
+constexpr int kGroups = kCgsThreads / kTile;   // 8
+constexpr int kMaxVec = 72;     // nv <= 72  (restart <= 71)
+constexpr int kAccPerWarp = (kMaxVec + kGroups - 1) / kGroups;
+
+// w_out = w_in - V[0..nv) hprev (if hprev); part[block][k] = sum conj(V_k) w_out (if dots);
+// part[block][nv] = sum |w_out|^2 (if norm).
+__global__ void __launch_bounds__(kCgsThreads)
+k_cgs(const double2* __restrict__ V, int nv, int64_t n, const double2* w_in, double2* w_out,
+      const double2* __restrict__ hprev, int do_dots, int do_norm, double2* __restrict__ part) {
+    extern __shared__ double2 sm[];
+    double2* sV = sm;                         // nv x kTile
+    double2* sw = sV + (size_t)nv * kTile;    // kTile
+    double2* sred = sw + kTile;               // kGroups x kTile
+    __shared__ double2 sh[kMaxVec];
+    const int t = threadIdx.x, e = t % kTile, g = t / kTile;
+    const int lane = t & 31, warp = t >> 5;
+    if (hprev)
+        for (int k = t; k < nv; k += blockDim.x) sh[k] = hprev[k];
+    double2 acc[kAccPerWarp];
+#pragma unroll
+    for (int a = 0; a < kAccPerWarp; a++) acc[a] = make_double2(0.0, 0.0);
+    double nacc = 0.0;
+    const int64_t ntiles = (n + kTile - 1) / kTile;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t base = tile * kTile;
+        const int64_t idx = base + e;
+        const bool ok = idx < n;
+        for (int k = g; k < nv; k += kGroups)
+            sV[k * kTile + e] = ok ? V[(int64_t)k * n + idx] : make_double2(0.0, 0.0);
+        if (g == 0) sw[e] = ok ? w_in[idx] : make_double2(0.0, 0.0);
+        __syncthreads();
+        if (hprev) {
+            double2 s = make_double2(0.0, 0.0);
+            for (int k = g; k < nv; k += kGroups) s = cfma(s, sV[k * kTile + e], sh[k]);
+            sred[g * kTile + e] = s;
+            __syncthreads();
+            if (g == 0) {
+                double2 tot = sred[e];
+#pragma unroll
+                for (int q = 1; q < kGroups; q++) tot = cadd(tot, sred[q * kTile + e]);
+                double2 wn = csub(sw[e], tot);
+                sw[e] = wn;
+                if (ok) w_out[idx] = wn;
+            }
+            __syncthreads();
+        }
+        if (do_dots) {
+            // warp `warp` owns vectors k = warp, warp + 8, ...; lane = element
+            const double2 we = sw[lane];
+#pragma unroll
+            for (int a = 0; a < kAccPerWarp; a++) {
+                const int k = warp + a * kGroups;
+                if (k < nv) {
+                    const double2 v = sV[k * kTile + lane];
+                    acc[a].x = fma(v.x, we.x, fma(v.y, we.y, acc[a].x));
+                    acc[a].y = fma(v.x, we.y, fma(-v.y, we.x, acc[a].y));
+                }
+            }
+        }
+        if (do_norm && g == 0) {
+            const double2 we = sw[e];
+            nacc = fma(we.x, we.x, fma(we.y, we.y, nacc));
+        }
+        __syncthreads();
+    }
+    const int stride = nv + 1;
+    if (do_dots) {
+#pragma unroll
+        for (int a = 0; a < kAccPerWarp; a++) {
+            const int k = warp + a * kGroups;
+            if (k < nv) {
+                double2 s = warp_sum2(acc[a]);
+                if (lane == 0) part[(int64_t)blockIdx.x * stride + k] = s;
+            }
+        }
+    }
+    if (do_norm && warp == 0) {
+        double s = warp_sum(nacc);
+        if (lane == 0) part[(int64_t)blockIdx.x * stride + nv] = make_double2(s, 0.0);
+    }
+}
+
+// out[k] = sum_b part[b][k], k < cnt; fixed-order tree per output (one block per k)
+__global__ void __launch_bounds__(256) k_reduce(const double2* __restrict__ part, int stride, int nblocks,
+                                                int koff, double2* __restrict__ out) {
+    const int k = blockIdx.x + koff;
+    __shared__ double2 s[256];
+    double2 a = make_double2(0.0, 0.0);
+    for (int b = threadIdx.x; b < nblocks; b += blockDim.x) a = cadd(a, part[(int64_t)b * stride + k]);
+    s[threadIdx.x] = a;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) s[threadIdx.x] = cadd(s[threadIdx.x], s[threadIdx.x + w]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[blockIdx.x] = s[0];
+}
+
+// Device GMRES state (one restart cycle).
+struct GState {
+    double2* H;     // (m+1) x m, column-major: H[i + (m+1) j]  (rotated, i.e. R)
+    double* cs;     // m
+    double2* sn;    // m
+    double2* g;     // m+1
+    double2* h1;    // m+2 (pass A output)
+    double2* h2;    // m+2 (pass B output + norm in [nv])
+    double2* nrm;   // 1   (pass C norm)
+    double2* y;     // m
+    double* scal;   // [0] |g_{j+1}|, [1] h_{j+1,j}, [2] 1/h_{j+1,j}, [3] breakdown flag
+};
+
+__device__ void givens_dev(double2 a, double2 b, double& c, double2& s, double2& r) {
+    const double aa = hypot(a.x, a.y), bb = hypot(b.x, b.y);
+    if (bb == 0.0) { c = 1.0; s = make_double2(0.0, 0.0); r = a; return; }
+    if (aa == 0.0) { c = 0.0; s = make_double2(1.0, 0.0); r = b; return; }
+    const double nu = hypot(aa, bb);
+    const double2 ph = make_double2(a.x / aa, a.y / aa);
+    c = aa / nu;
+    s = cscale(cmul(ph, cconj(b)), 1.0 / nu);
+    r = cscale(ph, nu);
+}
+
+// Hessenberg column j = h1 + h2, h_{j+1,j} = ||w||; rotate; update g.
+__global__ void k_arnoldi_step(GState st, int m, int j) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int ld = m + 1;
+    double2* Hj = st.H + (int64_t)ld * j;
+    for (int i = 0; i <= j; i++) Hj[i] = cadd(st.h1[i], st.h2[i]);
+    const double hn = sqrt(st.nrm[0].x);
+    double2 hnext = make_double2(hn, 0.0);
+    for (int i = 0; i < j; i++) {
+        const double c = st.cs[i];
+        const double2 s = st.sn[i];
+        const double2 t = cadd(cscale(Hj[i], c), cmul(s, Hj[i + 1]));
+        Hj[i + 1] = cadd(cscale(cmul(cconj(s), Hj[i]), -1.0), cscale(Hj[i + 1], c));
+        Hj[i] = t;
+    }
+    double c;
+    double2 s, r;
+    givens_dev(Hj[j], hnext, c, s, r);
+    st.cs[j] = c;
+    st.sn[j] = s;
+    Hj[j] = r;
+    Hj[j + 1] = make_double2(0.0, 0.0);
+    const double2 gj = st.g[j];
+    st.g[j + 1] = cscale(cmul(cconj(s), gj), -1.0);
+    st.g[j] = cscale(gj, c);
+    st.scal[0] = hypot(st.g[j + 1].x, st.g[j + 1].y);
+    st.scal[1] = hn;
+    st.scal[2] = hn > 0.0 ? 1.0 / hn : 0.0;
+    st.scal[3] = (r.x == 0.0 && r.y == 0.0) ? 1.0 : 0.0;
+}
+
+// y = R^{-1} g[0..k)
+__global__ void k_backsolve(GState st, int m, int k) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int ld = m + 1;
+    for (int i = k - 1; i >= 0; i--) {
+        double2 s = st.g[i];
+        for (int q = i + 1; q < k; q++) s = csub(s, cmul(st.H[i + (int64_t)ld * q], st.y[q]));
+        const double2 d = st.H[i + (int64_t)ld * i];
+        const double dd = d.x * d.x + d.y * d.y;
+        st.y[i] = cscale(cmul(s, cconj(d)), 1.0 / dd);
+    }
+}
+
+// x += sum_k V_k y_k
+__global__ void __launch_bounds__(256) k_update_x(const double2* __restrict__ V, int k, int64_t n,
+                                                  const double2* __restrict__ y, double2* x) {
+    __shared__ double2 sy[kMaxVec];
+    for (int q = threadIdx.x; q < k; q += blockDim.x) sy[q] = y[q];
+    __syncthreads();
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        double2 a = x[e];
+        for (int q = 0; q < k; q++) a = cfma(a, V[(int64_t)q * n + e], sy[q]);
+        x[e] = a;
+    }
+}
+
+// dst = src * scale, scale = *sptr (device scalar) or 1/sqrt(nrm) if from_norm
+__global__ void __launch_bounds__(256) k_scale(const double2* __restrict__ src, double2* dst, int64_t n,
+                                               const double* __restrict__ sptr, const double2* __restrict__ nrm) {
+    const double sc = sptr ? *sptr : 1.0 / sqrt(nrm->x);
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        dst[e] = cscale(src[e], sc);
+}
+
+// r = b - t
+__global__ void __launch_bounds__(256) k_sub(const double2* __restrict__ b, const double2* __restrict__ t,
+                                             double2* r, int64_t n) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        r[e] = csub(b[e], t[e]);
+}
+
+__global__ void k_init_cycle(GState st, int m, const double2* nrm) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    for (int i = 0; i <= m; i++) st.g[i] = make_double2(0.0, 0.0);
+    st.g[0] = make_double2(sqrt(nrm->x), 0.0);
+}
+
+// ---------------------------------------------------------------- host helpers
+struct Ctx {
+    Problem& P;
+    cudaStream_t s;
+    int64_t n;
+    int nblocks;
+    GState st;
+};
+
+int cgs_blocks(int64_t n) {
+    const int64_t ntiles = (n + kTile - 1) / kTile;
+    return (int)std::min<int64_t>(ntiles, (int64_t)kNumSMs * 6);
+}
+
+size_t cgs_smem(int nv) { return ((size_t)nv * kTile + kTile + (size_t)kGroups * kTile) * sizeof(double2); }
+
+void launch_cgs(Ctx& c, const double2* V, int nv, const double2* win, double2* wout, const double2* hprev,
+                bool dots, bool norm) {
+    size_t smem = cgs_smem(nv);
+    k_cgs<<<c.nblocks, kCgsThreads, smem, c.s>>>(V, nv, c.n, win, wout, hprev, dots ? 1 : 0, norm ? 1 : 0,
+                                                 c.P.K.part);
+    SSB_LAUNCHED();
+}
+
+void launch_reduce(Ctx& c, int stride, int koff, int cnt, double2* out) {
+    k_reduce<<<cnt, 256, 0, c.s>>>(c.P.K.part, stride, c.nblocks, koff, out);
+    SSB_LAUNCHED();
+}
+
+// ||v||^2 -> out (device double2, .x)
+void norm2(Ctx& c, const double2* v, double2* out) {
+    launch_cgs(c, nullptr, 0, v, nullptr, nullptr, false, true);
+    launch_reduce(c, 1, 0, 1, out);
+}
+
+void apply_precond(Problem& P, const double2* in, double2* out, double2* tmp, cudaStream_t s) {
+    trsv_lower(P.L, in, tmp, s);
+    trsv_upper(P.U, tmp, out, s);
+}
+
+int grid1(int64_t n) { return grid_for(n, 256, kNumSMs * 8); }
+
+}  // namespace
+
+void ensure_krylov(Problem& P, int m) {
+    Krylov& K = P.K;
+    if (K.m == m && K.n == P.n) return;
+    K.release();
+    K.m = m;
+    K.n = P.n;
+    const int64_t n = P.n;
+    SSB_CUDA(cudaMalloc(&K.V, (size_t)(m + 1) * n * sizeof(double2)));
+    SSB_CUDA(cudaMalloc(&K.w, n * sizeof(double2)));
+    SSB_CUDA(cudaMalloc(&K.t, n * sizeof(double2)));
+    SSB_CUDA(cudaMalloc(&K.x, n * sizeof(double2)));
+    SSB_CUDA(cudaMalloc(&K.b, n * sizeof(double2)));
+    SSB_CUDA(cudaMalloc(&K.r, n * sizeof(double2)));
+    const int nb = cgs_blocks(n);
+    K.part_cap = nb * (kMaxVec + 1);
+    SSB_CUDA(cudaMalloc(&K.part, (size_t)K.part_cap * sizeof(double2)));
+    // GState arrays packed in hcol
+    // H, sn, g, h1, h2, nrm, y, cs (as double2 slots), slack
+    const size_t words = (size_t)(m + 1) * m + m + (m + 1) + 2 * (m + 2) + 1 + m + m + 8;
+    SSB_CUDA(cudaMalloc(&K.hcol, words * sizeof(double2)));
+    SSB_CUDA(cudaMalloc(&K.scal, 8 * sizeof(double)));
+    SSB_CUDA(cudaHostAlloc(&K.h_stat, 8 * sizeof(double), cudaHostAllocDefault));
+    static bool attr_set = false;
+    if (!attr_set) {
+        SSB_CUDA(cudaFuncSetAttribute(k_cgs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cgs_smem(kMaxVec)));
+        attr_set = true;
+    }
+}
+
+void gmres_solve(Problem& P, const double2* b_dev, int m, double tol, int max_iter, ss_solve_info* info) {
+    SSB_CHECK(P.have_setup, SS_ERR_STATE, "ss_solve before ss_setup");
+    SSB_CHECK(m >= 1 && m + 1 <= kMaxVec, SS_ERR_ARG, "restart must be in [1, 71]");
+    SSB_CHECK(tol > 0.0 && max_iter >= 0, SS_ERR_ARG, "bad tol / max_iter");
+    ensure_krylov(P, m);
+    Krylov& K = P.K;
+    const int64_t n = P.n;
+    cudaStream_t s = P.stream;
+    Ctx c{P, s, n, cgs_blocks(n), {}};
+    double2* base = K.hcol;
+    c.st.H = base;
+    base += (size_t)(m + 1) * m;
+    c.st.sn = base;
+    base += m;
+    c.st.g = base;
+    base += m + 1;
+    c.st.h1 = base;
+    base += m + 2;
+    c.st.h2 = base;
+    base += m + 2;
+    c.st.nrm = base;
+    base += 1;
+    c.st.y = base;
+    base += m;
+    c.st.cs = reinterpret_cast<double*>(base);   // m doubles in m double2 slots
+    c.st.scal = K.scal;
+
+    SSB_CUDA(cudaEventRecord(P.ev0, s));
+    if (b_dev != K.b) SSB_CUDA(cudaMemcpyAsync(K.b, b_dev, n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+    SSB_CUDA(cudaMemsetAsync(K.x, 0, n * sizeof(double2), s));
+
+    // ||b||
+    norm2(c, K.b, c.st.nrm);
+    double2 hb;
+    SSB_CUDA(cudaMemcpyAsync(&hb, c.st.nrm, sizeof(double2), cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaStreamSynchronize(s));
+    const double bnorm = std::sqrt(hb.x);
+
+    int total = 0, cycles = 0, converged = 0;
+    double rel = 1.0;
+    if (bnorm == 0.0) {
+        converged = 1;
+        rel = 0.0;
+    }
+    while (!converged) {
+        // r = b - A x  (x = 0 on the first cycle -> r = b)
+        if (cycles == 0) {
+            SSB_CUDA(cudaMemcpyAsync(K.r, K.b, n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+        } else {
+            spmv(P.A, K.x, K.t, s);
+            k_sub<<<grid1(n), 256, 0, s>>>(K.b, K.t, K.r, n);
+            SSB_LAUNCHED();
+        }
+        norm2(c, K.r, c.st.nrm);
+        SSB_CUDA(cudaMemcpyAsync(&hb, c.st.nrm, sizeof(double2), cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaStreamSynchronize(s));
+        const double rn = std::sqrt(hb.x);
+        rel = rn / bnorm;
+        if (rel <= tol) {
+            converged = 1;
+            break;
+        }
+        if (total >= max_iter) break;
+        // z = M^{-1} r ; beta = ||z|| ; v0 = z / beta
+        apply_precond(P, K.r, K.w, K.t, s);
+        norm2(c, K.w, c.st.nrm);
+        k_init_cycle<<<1, 1, 0, s>>>(c.st, m, c.st.nrm);
+        SSB_LAUNCHED();
+        k_scale<<<grid1(n), 256, 0, s>>>(K.w, K.V, n, nullptr, c.st.nrm);
+        SSB_LAUNCHED();
+        SSB_CUDA(cudaMemcpyAsync(&hb, c.st.nrm, sizeof(double2), cudaMemcpyDeviceToHost, s));
+        SSB_CUDA(cudaStreamSynchronize(s));
+        const double beta = std::sqrt(hb.x);
+        if (!(beta > 0.0) || !std::isfinite(beta)) break;
+        const double target = beta * tol * bnorm / rn;
+        int k = 0;
+        for (int j = 0; j < m; j++) {
+            double2* vj = K.V + (int64_t)j * n;
+            spmv(P.A, vj, K.t, s);
+            apply_precond(P, K.t, K.w, K.r, s);
+            const int nv = j + 1;
+            // A: h1 = V^H w
+            launch_cgs(c, K.V, nv, K.w, K.w, nullptr, true, false);
+            launch_reduce(c, nv + 1, 0, nv, c.st.h1);
+            // B: w -= V h1 ; h2 = V^H w
+            launch_cgs(c, K.V, nv, K.w, K.w, c.st.h1, true, false);
+            launch_reduce(c, nv + 1, 0, nv, c.st.h2);
+            // C: w -= V h2 ; ||w||^2
+            launch_cgs(c, K.V, nv, K.w, K.w, c.st.h2, false, true);
+            launch_reduce(c, nv + 1, nv, 1, c.st.nrm);
+            k_arnoldi_step<<<1, 1, 0, s>>>(c.st, m, j);
+            SSB_LAUNCHED();
+            SSB_CUDA(cudaMemcpyAsync(K.h_stat, K.scal, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+            SSB_CUDA(cudaStreamSynchronize(s));
+            total++;
+            k = j + 1;
+            const double est = K.h_stat[0], hn = K.h_stat[1];
+            const bool breakdown = K.h_stat[3] != 0.0 || !(hn > 0.0) || !std::isfinite(est);
+            if (est <= target || total >= max_iter || breakdown || j == m - 1) break;
+            k_scale<<<grid1(n), 256, 0, s>>>(K.w, K.V + (int64_t)(j + 1) * n, n, K.scal + 2, nullptr);
+            SSB_LAUNCHED();
+        }
+        k_backsolve<<<1, 1, 0, s>>>(c.st, m, k);
+        SSB_LAUNCHED();
+        k_update_x<<<grid1(n), 256, 0, s>>>(K.V, k, n, c.st.y, K.x);
+        SSB_LAUNCHED();
+        cycles++;
+    }
+    SSB_CUDA(cudaEventRecord(P.ev1, s));
+    SSB_CUDA(cudaEventSynchronize(P.ev1));
+    float ms = 0.f;
+    SSB_CUDA(cudaEventElapsedTime(&ms, P.ev0, P.ev1));
+    if (info) {
+        info->iterations = total;
+        info->cycles = cycles;
+        info->converged = converged;
+        info->rel_residual = rel;
+        info->solve_ms = ms;
+    }
+}
+
+}  // namespace ssb

@@ -1,0 +1,157 @@
+// problem.h -- the handle behind ss_problem* and the internal interfaces.
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <vector>
+
+#include "../../include/ss_b200.h"
+#include "common.cuh"
+
+namespace ssb {
+
+// Device CSR matrix: int64 row pointers, int32 columns, complex128 values.
+struct DevCSR {
+    int64_t n = 0, nnz = 0;
+    int64_t* rowptr = nullptr;
+    int32_t* col = nullptr;
+    double2* val = nullptr;
+    void alloc_rowptr(int64_t n_) {
+        n = n_;
+        SSB_CUDA(cudaMalloc(&rowptr, (n + 1) * sizeof(int64_t)));
+    }
+    void alloc_entries(int64_t nnz_) {
+        nnz = nnz_;
+        SSB_CUDA(cudaMalloc(&col, (nnz > 0 ? nnz : 1) * sizeof(int32_t)));
+        SSB_CUDA(cudaMalloc(&val, (nnz > 0 ? nnz : 1) * sizeof(double2)));
+    }
+    void release() {
+        cudaFree(rowptr);
+        cudaFree(col);
+        cudaFree(val);
+        rowptr = nullptr;
+        col = nullptr;
+        val = nullptr;
+        n = nnz = 0;
+    }
+};
+
+// Host CSR (int64 everywhere) used during setup.
+struct HostCSR {
+    int64_t n = 0;
+    std::vector<int64_t> rowptr, col;
+    std::vector<double2> val;
+    int64_t nnz() const { return (int64_t)col.size(); }
+};
+
+// Triangular factor on the device in the layout the substitution kernel streams.
+struct DevTri {
+    int64_t n = 0, nnz = 0;       // strict (off-diagonal) entries
+    int64_t* rowptr = nullptr;    // strict part, rows in natural (RCM) order
+    int32_t* col = nullptr;
+    double2* val = nullptr;
+    double2* inv_diag = nullptr;  // U only: 1/u_ii
+    int64_t nlev = 0;
+    int64_t* lev_ptr = nullptr;   // level schedule: rows of level l are lev_rows[lev_ptr[l]..lev_ptr[l+1])
+    int32_t* lev_rows = nullptr;
+    void release() {
+        cudaFree(rowptr);
+        cudaFree(col);
+        cudaFree(val);
+        cudaFree(inv_diag);
+        cudaFree(lev_ptr);
+        cudaFree(lev_rows);
+        rowptr = nullptr;
+        col = nullptr;
+        val = nullptr;
+        inv_diag = nullptr;
+        lev_ptr = nullptr;
+        lev_rows = nullptr;
+        n = nnz = nlev = 0;
+    }
+};
+
+// GMRES(m) workspace.
+struct Krylov {
+    int m = 0;
+    int64_t n = 0;
+    double2* V = nullptr;      // (m+1) x n basis, row k = v_k
+    double2* w = nullptr;      // work vectors
+    double2* t = nullptr;
+    double2* x = nullptr;      // iterate (RCM order)
+    double2* b = nullptr;      // right-hand side (RCM order)
+    double2* r = nullptr;
+    double2* part = nullptr;   // block partial sums
+    int part_cap = 0;
+    double2* hcol = nullptr;   // device Hessenberg column accumulators (2 x (m+2))
+    double* scal = nullptr;    // device scalars
+    double* h_stat = nullptr;  // pinned host mirror of scalars
+    void release() {
+        cudaFree(V);
+        cudaFree(w);
+        cudaFree(t);
+        cudaFree(x);
+        cudaFree(b);
+        cudaFree(r);
+        cudaFree(part);
+        cudaFree(hcol);
+        cudaFree(scal);
+        if (h_stat) cudaFreeHost(h_stat);
+        *this = Krylov();
+    }
+};
+
+struct Problem {
+    ss_params params{};
+    cudaStream_t stream = nullptr;
+    int device = 0;
+    int64_t N = 0, n = 0, nnz = 0;
+    double2 w{0.0, 0.0};
+
+    DevCSR nat;                 // L~ natural order
+    DevCSR A;                   // L~_RCM
+    std::vector<int64_t> perm;  // new -> old
+    int64_t* d_perm = nullptr;
+    bool have_setup = false;
+
+    HostCSR hL, hU;             // host copies of the factors (export / tests)
+    DevTri L, U;
+    int64_t bw_nat = 0, bw_rcm = 0;
+
+    Krylov K;
+    double2* rho = nullptr;     // normalised solution, natural order (vec(rho))
+    bool have_solution = false;
+
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+    void release();
+};
+
+// build.cu
+void build_liouvillian(Problem& P);
+// setup.cpp
+void setup_problem(Problem& P, double drop_tol, double fill_factor, int threads, ss_setup_info* info);
+// rcm.cpp
+std::vector<int64_t> rcm_order(int64_t n, const std::vector<int64_t>& rowptr, const std::vector<int64_t>& col);
+// ilut.cpp
+struct IlutStats {
+    int32_t repaired = 0;
+    int32_t threads = 1;
+};
+void ilut_factor(const HostCSR& A, double drop_tol, double fill_factor, int threads, HostCSR& L,
+                 HostCSR& U, IlutStats& st);
+// spmv.cu
+void spmv(const DevCSR& A, const double2* x, double2* y, cudaStream_t s);
+// trsv.cu
+void trsv_lower(const DevTri& L, const double2* b, double2* x, cudaStream_t s);
+void trsv_upper(const DevTri& U, const double2* b, double2* x, cudaStream_t s);
+// krylov.cu / gmres.cu
+void gmres_solve(Problem& P, const double2* b_dev, int restart, double tol, int max_iter,
+                 ss_solve_info* info);
+void finish_solution(Problem& P, ss_solve_info* info);
+void expectations(Problem& P, double* na, double* nb);
+void gather_perm(const double2* src, const int64_t* perm, int64_t n, double2* dst, cudaStream_t s);   // dst[k] = src[perm[k]]
+void scatter_perm(const double2* src, const int64_t* perm, int64_t n, double2* dst, cudaStream_t s);  // dst[perm[k]] = src[k]
+void ensure_krylov(Problem& P, int m);
+
+}  // namespace ssb
