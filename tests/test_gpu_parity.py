@@ -1,0 +1,178 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element.
+
+Bars: index work (structure, permutation, factor patterns)
+bit-exact; assembled values and ILUT values bit-exact (same IEEE operations in the
+same order, no FMA); SpMV / substitutions within a rounding-order tolerance; the
+steady state within the north-star tolerances ||rho_gpu - rho_oracle||_1 <= 1e-6,
+||L rho|| / ||b|| <= 1e-9, |Tr rho - 1| <= 1e-12.
+"""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from oracle import ilut as I
+from oracle import liouvillian as lv
+from oracle import rcm as R
+from oracle import steadystate as ss
+from oracle import trisolve as T
+from workloads import CONFIGS, jittered, rand_cvec, tiny_params
+
+pytestmark = pytest.mark.gpu
+
+
+def pb():
+    import paper_1411_4356_b200 as m
+    return m
+
+
+EDGE = {
+    "Nc1": tiny_params(1, 6),                       # no cavity dynamics
+    "Nm1": tiny_params(5, 1),                       # no mechanics
+    "nth0": tiny_params(3, 7, n_th=0.0),            # D[b^+] absent
+    "E0": tiny_params(3, 5, E=0.0),
+    "g00": tiny_params(4, 5, g0=0.0),
+    "Delta0": tiny_params(3, 6, Delta=0.0),
+    "w_given": tiny_params(3, 4, w=2.5),
+    "ragged": tiny_params(7, 13, Delta=0.37, g0=0.55),
+}
+BUILD_CASES = {**{k: CONFIGS[k] for k in ("tiny", "small")}, **EDGE,
+               "jit1": jittered(CONFIGS["small"], 11), "jit2": jittered(CONFIGS["tiny"], 12)}
+
+
+@pytest.mark.parametrize("name", list(BUILD_CASES))
+def test_build_bit_exact(cuda, name):
+    p = BUILD_CASES[name]
+    s = pb().SteadyState(p)
+    Lt, _, w, _ = lv.constrained_system(p)
+    rp, ci, va = pb().ss_export_matrix(s.handle, 0)
+    assert np.array_equal(rp, Lt.indptr) and np.array_equal(ci, Lt.indices)
+    assert np.array_equal(va, Lt.data)                      # bit-exact values (+0/-0 compare equal)
+    assert complex(s.build_info["w_re"], s.build_info["w_im"]) == w
+    s.close()
+
+
+@pytest.mark.parametrize("name", ["tiny", "small", "ragged", "nth0", "Nc1"])
+def test_setup_bit_exact(cuda, name):
+    p = {**CONFIGS, **EDGE}[name]
+    s = pb().SteadyState(p).setup()
+    Lt, _, _, _ = lv.constrained_system(p)
+    perm = ss.rcm_c(R.symmetrized_pattern(Lt))
+    assert np.array_equal(pb().ss_export_perm(s.handle), perm)
+    if Lt.shape[0] <= 2000:
+        assert np.array_equal(R.rcm(R.symmetrized_pattern(Lt)), perm)
+    A = R.permute(Lt, perm)
+    rp, ci, va = pb().ss_export_matrix(s.handle, 1)
+    assert np.array_equal(rp, A.indptr) and np.array_equal(ci, A.indices) and np.array_equal(va, A.data)
+    F = I.ilut(A, p.drop_tol, p.fill_factor)
+    for which, (P_, J_, X_) in ((0, (F.Lp, F.Lj, F.Lx)), (1, (F.Up, F.Uj, F.Ux))):
+        gp, gj, gx = pb().ss_export_factors(s.handle, which)
+        assert np.array_equal(gp, P_) and np.array_equal(gj, J_)
+        assert np.array_equal(gx, X_)
+    assert s.setup_info["nnz_L"] + s.setup_info["nnz_U"] == F.nnz
+    s.close()
+
+
+@pytest.mark.parametrize("name", ["tiny", "small", "ragged"])
+def test_spmv_and_substitutions(cuda, name):
+    torch = cuda
+    p = {**CONFIGS, **EDGE}[name]
+    s = pb().SteadyState(p).setup()
+    Lt, _, _, _ = lv.constrained_system(p)
+    perm = pb().ss_export_perm(s.handle)
+    A = R.permute(Lt, perm)
+    F = I.ilut(A, p.drop_tol, p.fill_factor)
+    n = A.shape[0]
+    for seed in (1, 2):
+        x = rand_cvec(n, seed)
+        xd = torch.from_numpy(x).cuda()
+        y = s.spmv(xd).cpu().numpy()
+        ref = A @ x
+        assert np.abs(y - ref).max() <= 1e-13 * np.abs(ref).max()
+        Lm = T.lower_unit_matrix(F)
+        yl = s.precond(xd, 0).cpu().numpy()
+        rl = sp.linalg.spsolve_triangular(Lm, x, lower=True, unit_diagonal=True)
+        assert np.abs(yl - rl).max() <= 1e-11 * np.abs(rl).max()
+        yu = s.precond(xd, 1).cpu().numpy()
+        ru = sp.linalg.spsolve_triangular(F.U(), x, lower=False)
+        assert np.abs(yu - ru).max() <= 1e-11 * np.abs(ru).max()
+        ym = s.precond(xd, 2).cpu().numpy()
+        rm = T.apply_preconditioner(F, x)
+        assert np.abs(ym - rm).max() <= 1e-10 * np.abs(rm).max()
+    s.close()
+
+
+@pytest.mark.parametrize("name", ["tiny", "small", "ragged", "nth0", "g00", "w_given"])
+def test_steady_state_parity(cuda, name):
+    p = {**CONFIGS, **EDGE}[name]
+    s = pb().SteadyState(p).setup().solve()
+    info = s.solve_info
+    assert info["converged"] == 1 and info["rel_residual"] <= p.tol
+    rho = s.rho().cpu().numpy()
+    ref = ss.solve_direct(p)
+    assert np.abs(rho - ref).sum() <= 1e-6
+    assert ss.liouvillian_residual(rho, p) <= 1e-9
+    assert abs(np.trace(rho) - 1) <= 1e-12
+    na, nb = s.expect()
+    ra, rb = ss.expect(ref, p)
+    assert abs(na - ra) <= 1e-8 and abs(nb - rb) <= 1e-8
+    # same algorithm as the oracle: iteration counts agree closely (CGS2 vs MGS rounding)
+    it = ss.solve_iterative(p)
+    assert abs(info["iterations"] - it.gmres.iterations) <= max(2, it.gmres.iterations // 10)
+    s.close()
+
+
+def test_solve_host_e2e(cuda):
+    p = CONFIGS["small"]
+    s = pb().SteadyState(p).setup()
+    n = s.n
+    x = np.empty(n, np.complex128)
+    info = pb().ss_solve_host(s.handle, None, x.ctypes.data, p.restart, p.tol, p.max_iter)
+    assert info["converged"] == 1
+    rho = lv.unvec(x, p.hilbert_dim)
+    rho = rho / np.trace(rho)
+    assert np.abs(rho - ss.solve_direct(p)).sum() <= 1e-6
+    # arbitrary right-hand side through host buffers: L~ x = r
+    Lt, _, _, _ = lv.constrained_system(p)
+    r = rand_cvec(n, 5)
+    info = pb().ss_solve_host(s.handle, r.ctypes.data, x.ctypes.data, 50, 1e-11, 3000)
+    assert info["converged"] == 1
+    assert np.linalg.norm(Lt @ x - r) / np.linalg.norm(r) <= 1e-11
+    s.close()
+
+
+def test_errors_are_reported(cuda):
+    m = pb()
+    h, _ = m.ss_build(CONFIGS["tiny"])
+    with pytest.raises(m.SSError) as e:
+        m.ss_solve(h, 30, 1e-10, 100)
+    assert e.value.code == 5
+    m.ss_setup(h, 1e-4, 20)
+    with pytest.raises(m.SSError) as e:
+        m.ss_solve(h, 0, 1e-10, 100)
+    assert e.value.code == 1
+    with pytest.raises(m.SSError):
+        m.ss_setup(h, -1.0, 20)
+    m.ss_destroy(h)
+    bad = CONFIGS["tiny"].with_(kappa=-1.0)
+    with pytest.raises(m.SSError) as e:
+        m.ss_build(bad)
+    assert e.value.code == 1
+
+
+def test_zero_pivot_breakdown_reported(cuda):
+    """d = 0 with an exactly singular pivot cannot be repaired (R6): SS_ERR_BREAKDOWN."""
+    m = pb()
+    p = tiny_params(1, 2, kappa=0.0, Gamma_m=0.0, n_th=0.0, g0=0.0, E=0.0, Delta=0.0, omega_m=0.0, w=1.0)
+    h, _ = m.ss_build(p)      # L = 0: L~ = T only -> singular
+    with pytest.raises(m.SSError) as e:
+        m.ss_setup(h, 0.0, 10)
+    assert e.value.code == 4
+    m.ss_destroy(h)
+
+
+def test_kernel_launch_counter_moves(cuda):
+    m = pb()
+    before = m.ss_kernel_launches()
+    s = m.SteadyState(CONFIGS["tiny"]).setup().solve()
+    assert m.ss_kernel_launches() > before + 10
+    s.close()

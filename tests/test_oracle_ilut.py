@@ -1,0 +1,132 @@
+"""Oracle pins for the dual-threshold ILU (sec. II) and the condition estimate (sec. IV)."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from oracle import ilut as I
+from oracle import trisolve as T
+
+
+def rand_dd(n, density, seed, complex_=True):
+    rng = np.random.default_rng(seed)
+    A = sp.random(n, n, density=density, random_state=seed, format="csr")
+    if complex_:
+        B = sp.random(n, n, density=density, random_state=seed + 100, format="csr")
+        A = A + 1j * B
+    A = A + sp.diags(4.0 + rng.random(n) + 1j * rng.random(n))
+    A = sp.csr_matrix(A)
+    A.sort_indices()
+    return A
+
+
+def full_LU(F):
+    L = (F.L() + sp.identity(F.n)).toarray()
+    U = F.U().toarray()
+    return L, U
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_d0_unbounded_fill_is_complete_lu(seed):
+    """'In the limit where d=0, the iLU preconditioner returns the complete LU factorization'.
+    A unit-lower/upper LU without pivoting is unique, so L U = A pins every entry."""
+    A = rand_dd(40, 0.1, seed)
+    F = I.ilut(A, 0.0, 1e9)
+    L, U = full_LU(F)
+    assert np.allclose(np.tril(L, -1), L - np.eye(40)) and np.allclose(np.triu(U), U)
+    assert np.abs(L @ U - A.toarray()).max() <= 1e-12 * np.abs(A).max()
+    x = np.random.default_rng(seed).standard_normal(40) + 0j
+    assert np.abs(T.apply_preconditioner(F, A @ x, small_loops=True) - x).max() < 1e-12
+
+
+def test_identity():
+    F = I.ilut(sp.identity(5, dtype=complex, format="csr"), 1e-3, 10)
+    assert F.Lj.size == 0 and np.array_equal(F.Uj, np.arange(5)) and np.allclose(F.Ux, 1)
+
+
+def test_lower_triangular_input_is_exact():
+    """ILUT of a lower-triangular matrix with no fill: l_ij = a_ij / a_jj, U = diag(A) (for d = 0)."""
+    A = sp.csr_matrix(np.array([[2, 0, 0], [1, 4, 0], [0, 3, 5.0]], dtype=complex))
+    F = I.ilut(A, 0.0, 100)
+    L, U = full_LU(F)
+    assert np.allclose(L, [[1, 0, 0], [0.5, 1, 0], [0, 0.75, 1]]) and np.allclose(U, np.diag([2, 4, 5]))
+
+
+def test_tridiagonal_no_fill():
+    n = 12
+    A = sp.diags([np.full(n - 1, 1.0), np.full(n, 4.0), np.full(n - 1, 1.0 + 1j)], [-1, 0, 1], format="csr",
+                 dtype=complex)
+    F = I.ilut(A, 1e-12, 10)
+    assert F.nnz == A.nnz
+    L, U = full_LU(F)
+    assert np.abs(L @ U - A.toarray()).max() < 1e-14
+
+
+def test_hand_worked_drop():
+    """3x3 with d = 0.01 (worked by hand, R4-R5):
+    row 2: multiplier 0.001/4 = 2.5e-4 < 0.01*4 -> dropped, no update; multiplier 1/3.75 kept."""
+    A = sp.csr_matrix(np.array([[4, 1, 0], [1, 4, 1], [0.001, 1, 4]], dtype=complex))
+    F = I.ilut(A, 0.01, 100)
+    L, U = full_LU(F)
+    u11 = 4 - 0.25
+    l21 = 1.0 / u11
+    assert np.allclose(L, [[1, 0, 0], [0.25, 1, 0], [0, l21, 1]], rtol=0, atol=1e-15)
+    assert np.allclose(U, [[4, 1, 0], [0, u11, 1], [0, 0, 4 - l21]], rtol=0, atol=1e-15)
+    # the complete factorisation keeps the small multiplier
+    Fe = I.ilut(A, 0.0, 100)
+    assert abs(full_LU(Fe)[0][2, 0] - 0.001 / 4) < 1e-18
+
+
+def test_fill_cap_keeps_largest():
+    """p caps each part of a row at floor(p nnz(a_i) / 2) entries, the largest |.|."""
+    n = 6
+    dense = np.eye(n, dtype=complex) * 10
+    dense[5, :5] = [1, 5, 2, 4, 3]          # L part of row 5 (no fill from rows 0-4: they are diagonal)
+    dense[0, 1:] = [3, 1, 4, 1, 5]          # U part of row 0
+    A = sp.csr_matrix(dense)
+    F = I.ilut(A, 0.0, 0.7)                 # row 5: nnz 6 -> lfil = floor(0.7*6/2) = 2
+    L = F.L().toarray()
+    assert np.count_nonzero(L[5]) == 2 and set(np.nonzero(L[5])[0]) == {1, 3}
+    U = F.U().toarray()
+    assert set(np.nonzero(U[0, 1:])[0] + 1) == {3, 5} and U[0, 0] == 10
+
+
+def test_drop_rule_and_cap_on_random():
+    A = rand_dd(200, 0.05, 3)
+    d, p = 0.05, 3.0
+    F = I.ilut(A, d, p)
+    rowmax = abs(A).max(axis=1).toarray().ravel()
+    nnz_row = np.diff(A.indptr)
+    for i in range(200):
+        lv = F.Lx[F.Lp[i]:F.Lp[i + 1]]
+        uv = F.Ux[F.Up[i] + 1:F.Up[i + 1]]
+        lfil = int(p * nnz_row[i] / 2)
+        assert len(lv) <= lfil and len(uv) <= lfil
+        assert np.all(np.abs(lv) >= d * rowmax[i] * (1 - 1e-15))
+        assert np.all(np.abs(uv) >= d * rowmax[i] * (1 - 1e-15))
+    assert F.nnz <= p * A.nnz + 200
+
+
+def test_zero_pivot_repair_and_error():
+    A = sp.csr_matrix(np.array([[1, 1], [1, 1.0]], dtype=complex))
+    F = I.ilut(A, 0.1, 10)
+    assert F.diag()[1] == 0.1
+    with pytest.raises(RuntimeError):
+        I.ilut(A, 0.0, 10)
+
+
+def test_condest():
+    """condition estimate ||M e||_inf (reading R8: (LU)^{-1} e)."""
+    F = I.ilut(sp.identity(4, dtype=complex, format="csr"), 0.0, 10)
+    assert I.condest(F) == 1.0
+    F = I.ilut(sp.diags([1.0, 1e-8]).tocsr().astype(complex), 0.0, 10)
+    assert abs(I.condest(F) - 1e8) < 1e-6
+
+
+def test_triangular_solves_against_dense():
+    A = rand_dd(60, 0.1, 11)
+    F = I.ilut(A, 1e-3, 5)
+    L, U = full_LU(F)
+    b = np.random.default_rng(2).standard_normal(60) + 1j
+    ref = np.linalg.solve(U, np.linalg.solve(L, b))
+    assert np.abs(T.apply_preconditioner(F, b, small_loops=True) - ref).max() < 1e-11
+    assert np.abs(T.apply_preconditioner(F, b) - ref).max() < 1e-11
