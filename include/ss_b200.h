@@ -80,6 +80,8 @@ typedef struct ss_setup_info {
     int64_t levels_U;
     int32_t pivots_repaired;/* zero pivots replaced by tau_i (reading R6)                     */
     int32_t threads;        /* host threads used by the factorisation                        */
+    int32_t trsv_block;     /* rows per block B of the block substitution (trsv.cu)          */
+    int32_t trsv_grid;      /* persistent CTAs of the block substitution (0 before first use) */
     double rcm_ms, ilut_ms, upload_ms;
 } ss_setup_info;
 
@@ -153,6 +155,14 @@ int ss_spmv(ss_problem* h, const void* x_dev, void* y_dev);
 /* y = L^{-1} x (which = 0), y = U^{-1} x (which = 1), y = U^{-1} L^{-1} x (which = 2);
  * device pointers, length n, x and y may not alias.                                */
 int ss_precond(ss_problem* h, int32_t which, const void* x_dev, void* y_dev);
+
+/* Diagnostic: run the block substitution of factor `which` (0 = L, 1 = U) on x_dev -> y_dev
+ * (device pointers, length n) with per-block %globaltimer stamps (ns) copied to host_trace
+ * [8 * nblk]: block start, warp-0 far part done, all far parts done, near part done, x
+ * stored, flag released, inverse block staged, mat-vec done.  *nblk_out receives the
+ * number of blocks (host_trace may be NULL to query it). */
+int ss_debug_trace_trsv(ss_problem* h, int32_t which, const void* x_dev, void* y_dev, uint64_t* host_trace,
+                        int64_t* nblk_out);
 
 /* Number of CUDA kernels this library has launched since load (gpu_launches evidence). */
 int64_t ss_kernel_launches(void);

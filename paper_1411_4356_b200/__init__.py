@@ -13,11 +13,11 @@ from __future__ import annotations
 from . import _lib
 from ._lib import (SSError, ss_build, ss_setup, ss_solve, ss_expect, ss_get_rho, ss_solve_host,
                    ss_destroy, ss_sizes, ss_export_matrix, ss_export_perm, ss_export_factors, ss_spmv,
-                   ss_precond, ss_kernel_launches)
+                   ss_precond, ss_kernel_launches, ss_debug_trace_trsv)
 
 __all__ = ["SteadyState", "SSError", "ss_build", "ss_setup", "ss_solve", "ss_expect", "ss_get_rho",
            "ss_solve_host", "ss_destroy", "ss_sizes", "ss_export_matrix", "ss_export_perm",
-           "ss_export_factors", "ss_spmv", "ss_precond", "ss_kernel_launches"]
+           "ss_export_factors", "ss_spmv", "ss_precond", "ss_kernel_launches", "ss_debug_trace_trsv"]
 
 
 class SteadyState:

@@ -43,6 +43,7 @@ class ss_setup_info(ctypes.Structure):
                 ("bandwidth_nat", ctypes.c_int64), ("bandwidth_rcm", ctypes.c_int64),
                 ("levels_L", ctypes.c_int64), ("levels_U", ctypes.c_int64),
                 ("pivots_repaired", ctypes.c_int32), ("threads", ctypes.c_int32),
+                ("trsv_block", ctypes.c_int32), ("trsv_grid", ctypes.c_int32),
                 ("rcm_ms", ctypes.c_double), ("ilut_ms", ctypes.c_double), ("upload_ms", ctypes.c_double)]
 
 
@@ -77,6 +78,7 @@ SIGNATURES = [
     ("ss_spmv", ctypes.c_int, [P, P, P]),
     ("ss_precond", ctypes.c_int, [P, I32, P, P]),
     ("ss_kernel_launches", ctypes.c_int64, []),
+    ("ss_debug_trace_trsv", ctypes.c_int, [P, I32, P, P, P, PI64]),
 ]
 
 _lib = None
@@ -191,6 +193,15 @@ def ss_spmv(h, x_dev_ptr: int, y_dev_ptr: int):
 
 def ss_precond(h, which: int, x_dev_ptr: int, y_dev_ptr: int):
     _check(load().ss_precond(h, int(which), P(x_dev_ptr), P(y_dev_ptr)))
+
+
+def ss_debug_trace_trsv(h, which: int, x_dev_ptr: int, y_dev_ptr: int) -> np.ndarray:
+    """Per-block globaltimer stamps (ns), shape (nblk, 8); see include/ss_b200.h."""
+    nb = ctypes.c_int64()
+    _check(load().ss_debug_trace_trsv(h, int(which), P(x_dev_ptr), P(y_dev_ptr), None, ctypes.byref(nb)))
+    tr = np.empty((nb.value, 8), np.uint64)
+    _check(load().ss_debug_trace_trsv(h, int(which), P(x_dev_ptr), P(y_dev_ptr), tr.ctypes.data, ctypes.byref(nb)))
+    return tr
 
 
 def ss_kernel_launches() -> int:

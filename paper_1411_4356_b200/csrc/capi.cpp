@@ -246,18 +246,43 @@ int ss_precond(ss_problem* h, int32_t which, const void* x_dev, void* y_dev) {
     const double2* x = (const double2*)x_dev;
     double2* y = (double2*)y_dev;
     if (which == 0) {
-        trsv_lower(P.L, x, y, P.stream);
+        block_trsv(P.L, x, y, P.stream);
     } else if (which == 1) {
-        trsv_upper(P.U, x, y, P.stream);
+        block_trsv(P.U, x, y, P.stream);
     } else {
         double2* tmp = nullptr;
         SSB_CUDA(cudaMalloc(&tmp, P.n * sizeof(double2)));
-        trsv_lower(P.L, x, tmp, P.stream);
-        trsv_upper(P.U, tmp, y, P.stream);
+        block_trsv(P.L, x, tmp, P.stream);
+        block_trsv(P.U, tmp, y, P.stream);
         SSB_CUDA(cudaStreamSynchronize(P.stream));
         cudaFree(tmp);
     }
     SSB_CUDA(cudaStreamSynchronize(P.stream));
+    SS_GUARD_END
+}
+
+int ss_debug_trace_trsv(ss_problem* h, int32_t which, const void* x_dev, void* y_dev, uint64_t* host_trace,
+                        int64_t* nblk_out) {
+    SS_GUARD_BEGIN
+    SSB_CHECK(h && x_dev && y_dev && x_dev != y_dev && nblk_out, SS_ERR_ARG, "ss_debug_trace_trsv: bad pointers");
+    SSB_CHECK(which == 0 || which == 1, SS_ERR_ARG, "ss_debug_trace_trsv: which must be 0 or 1");
+    Problem& P = h->P;
+    SSB_CHECK(P.have_setup, SS_ERR_STATE, "ss_debug_trace_trsv before ss_setup");
+    DevBlockTri& T = which == 0 ? P.L : P.U;
+    *nblk_out = T.nblk;
+    if (!host_trace) return SS_OK;
+    unsigned long long* d = nullptr;
+    SSB_CUDA(cudaMalloc(&d, T.nblk * 8 * sizeof(unsigned long long)));
+    try {
+        block_trsv(T, (const double2*)x_dev, (double2*)y_dev, P.stream, d);
+        SSB_CUDA(cudaMemcpyAsync(host_trace, d, T.nblk * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                 P.stream));
+        SSB_CUDA(cudaStreamSynchronize(P.stream));
+    } catch (...) {
+        cudaFree(d);
+        throw;
+    }
+    cudaFree(d);
     SS_GUARD_END
 }
 

@@ -262,8 +262,8 @@ void norm2(Ctx& c, const double2* v, double2* out) {
 }
 
 void apply_precond(Problem& P, const double2* in, double2* out, double2* tmp, cudaStream_t s) {
-    trsv_lower(P.L, in, tmp, s);
-    trsv_upper(P.U, tmp, out, s);
+    block_trsv(P.L, in, tmp, s);
+    block_trsv(P.U, tmp, out, s);
 }
 
 int grid1(int64_t n) { return grid_for(n, 256, kNumSMs * 8); }

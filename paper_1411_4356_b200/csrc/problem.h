@@ -44,30 +44,46 @@ struct HostCSR {
     int64_t nnz() const { return (int64_t)col.size(); }
 };
 
-// Triangular factor on the device in the layout the substitution kernel streams.
-struct DevTri {
-    int64_t n = 0, nnz = 0;       // strict (off-diagonal) entries
-    int64_t* rowptr = nullptr;    // strict part, rows in natural (RCM) order
-    int32_t* col = nullptr;
-    double2* val = nullptr;
-    double2* inv_diag = nullptr;  // U only: 1/u_ii
-    int64_t nlev = 0;
-    int64_t* lev_ptr = nullptr;   // level schedule: rows of level l are lev_rows[lev_ptr[l]..lev_ptr[l+1])
-    int32_t* lev_rows = nullptr;
+// Triangular factor on the device in the block layout of trsv.cu (kernel index space:
+// L as is, U reversed i' = n-1-i so that both are lower triangular).
+struct TriArgs {
+    int64_t n, nblk;
+    int32_t rev, B;
+    const int64_t* farptr;    // [n+1] entries of row i' with source block <= k-3 (k = i'/B)
+    const int32_t* fcol;      //       kernel-space columns, ascending within a row
+    const double2* fval;
+    const int64_t* nrp;       // [n+1] entries of row i' with source block k-2 or k-1
+    const int32_t* ncol;
+    const double2* nval;
+    const double2* dinv;      // [nblk][B(B+1)/2] inverse diagonal blocks, packed lower, column-major
+    uint32_t* flags;          // [nblk] completion flags (value = launch epoch)
+};
+
+struct DevBlockTri {
+    int64_t n = 0, nblk = 0, nnz_far = 0, nnz_near = 0, nnz_strict = 0;
+    int B = 0, rev = 0, nt = 0;   // rows per block, reversed (U), threads per CTA
+    int64_t* farptr = nullptr;
+    int32_t* fcol = nullptr;
+    double2* fval = nullptr;
+    int64_t* nrp = nullptr;
+    int32_t* ncol = nullptr;
+    double2* nval = nullptr;
+    double2* dinv = nullptr;
+    uint32_t* flags = nullptr;
+    uint32_t epoch = 0;
+    int grid = 0;
+    int64_t nlev = 0;   // row-level dependency levels (diagnostic)
+    TriArgs args() const { return TriArgs{n, nblk, rev, B, farptr, fcol, fval, nrp, ncol, nval, dinv, flags}; }
     void release() {
-        cudaFree(rowptr);
-        cudaFree(col);
-        cudaFree(val);
-        cudaFree(inv_diag);
-        cudaFree(lev_ptr);
-        cudaFree(lev_rows);
-        rowptr = nullptr;
-        col = nullptr;
-        val = nullptr;
-        inv_diag = nullptr;
-        lev_ptr = nullptr;
-        lev_rows = nullptr;
-        n = nnz = nlev = 0;
+        cudaFree(farptr);
+        cudaFree(fcol);
+        cudaFree(fval);
+        cudaFree(nrp);
+        cudaFree(ncol);
+        cudaFree(nval);
+        cudaFree(dinv);
+        cudaFree(flags);
+        *this = DevBlockTri();
     }
 };
 
@@ -115,7 +131,7 @@ struct Problem {
     bool have_setup = false;
 
     HostCSR hL, hU;             // host copies of the factors (export / tests)
-    DevTri L, U;
+    DevBlockTri L, U;
     int64_t bw_nat = 0, bw_rcm = 0;
 
     Krylov K;
@@ -142,9 +158,13 @@ void ilut_factor(const HostCSR& A, double drop_tol, double fill_factor, int thre
                  HostCSR& U, IlutStats& st);
 // spmv.cu
 void spmv(const DevCSR& A, const double2* x, double2* y, cudaStream_t s);
-// trsv.cu
-void trsv_lower(const DevTri& L, const double2* b, double2* x, cudaStream_t s);
-void trsv_upper(const DevTri& U, const double2* b, double2* x, cudaStream_t s);
+// trsv.cu: x = T^{-1} b for one factor (b, x in natural index order; x must not alias b)
+// trace (optional, device, 8 x nblk globaltimer stamps per block): start, warp-0 far
+// done, all far done, near done, x stored, flag released, inverse staged, mat-vec done.
+void block_trsv(DevBlockTri& T, const double2* b, double2* x, cudaStream_t s,
+                unsigned long long* trace = nullptr);
+size_t block_trsv_packed(int B);
+void block_trsv_prepare(DevBlockTri& T);   // launch geometry (persistent grid)
 // krylov.cu / gmres.cu
 void gmres_solve(Problem& P, const double2* b_dev, int restart, double tol, int max_iter,
                  ss_solve_info* info);

@@ -7,7 +7,9 @@
 // sec. II: ILUT(d, p).
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
+#include <thread>
 
 #include "problem.h"
 
@@ -81,15 +83,26 @@ HostCSR permute(const HostCSR& A, const std::vector<int64_t>& perm) {
     return B;
 }
 
-// Level schedule of a triangular dependency graph given as strict rows.
-// lower: level(i) = 1 + max level(j), j < i in row i; upper: processed from the bottom.
-void levels(const std::vector<int64_t>& rp, const std::vector<int64_t>& col, int64_t n, bool upper,
-            int64_t skip_first, std::vector<int64_t>& lev_ptr, std::vector<int32_t>& lev_rows) {
+template <class Fn>
+void parallel_for(int64_t n, int threads, Fn fn, int64_t grain = 1024) {
+    threads = (int)std::max<int64_t>(1, std::min<int64_t>(threads, n / grain + 1));
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; t++) {
+        const int64_t lo = n * t / threads, hi = n * (t + 1) / threads;
+        pool.emplace_back([=, &fn] { fn(lo, hi); });
+    }
+    for (auto& th : pool) th.join();
+}
+
+// Row-level dependency levels of the substitution (diagnostic: the length of the
+// chain a row-level schedule would walk).
+int64_t count_levels(const HostCSR& F, bool upper) {
+    const int64_t n = F.n;
     std::vector<int32_t> lev(n, 0);
     int32_t maxl = 0;
     auto row = [&](int64_t i) {
         int32_t l = 0;
-        for (int64_t q = rp[i] + skip_first; q < rp[i + 1]; q++) l = std::max(l, lev[col[q]] + 1);
+        for (int64_t q = F.rowptr[i] + (upper ? 1 : 0); q < F.rowptr[i + 1]; q++) l = std::max(l, lev[F.col[q]] + 1);
         lev[i] = l;
         maxl = std::max(maxl, l);
     };
@@ -97,65 +110,175 @@ void levels(const std::vector<int64_t>& rp, const std::vector<int64_t>& col, int
         for (int64_t i = 0; i < n; i++) row(i);
     else
         for (int64_t i = n - 1; i >= 0; i--) row(i);
-    lev_ptr.assign((size_t)maxl + 2, 0);
-    for (int64_t i = 0; i < n; i++) lev_ptr[lev[i] + 1]++;
-    for (int32_t l = 0; l <= maxl; l++) lev_ptr[l + 1] += lev_ptr[l];
-    lev_rows.resize(n);
-    std::vector<int64_t> pos(lev_ptr.begin(), lev_ptr.end() - 1);
-    if (!upper)
-        for (int64_t i = 0; i < n; i++) lev_rows[pos[lev[i]]++] = (int32_t)i;
-    else
-        for (int64_t i = n - 1; i >= 0; i--) lev_rows[pos[lev[i]]++] = (int32_t)i;
+    return n ? (int64_t)maxl + 1 : 0;
 }
 
-void upload_tri(const HostCSR& F, bool upper, DevTri& T, cudaStream_t s) {
+// Block layout of one ILU factor for trsv.cu.  Kernel index space: L as is; U reversed
+// (i' = n-1-i), which turns the upper factor into a lower one.  Row i' of block k splits
+// its strict entries (ascending kernel column) into "far" (column < (k-2)B), "near"
+// ((k-2)B <= column < kB) and in-block; far and near go to two CSR arrays, the in-block
+// entries and the diagonal (1 for L, u_ii for U) form the dense block D_k, whose
+// inverse is stored packed (lower, column-major; column j = rows j..B-1).  The last
+// block is padded with identity rows.
+void build_block_tri(const HostCSR& F, bool upper, int B, int nt, int threads, DevBlockTri& T, cudaStream_t s) {
     T.release();
+    T.nt = nt;
     const int64_t n = F.n;
+    const int64_t nblk = (n + B - 1) / B;
+    const int64_t PK = (int64_t)block_trsv_packed(B);
     T.n = n;
-    // strict part (U: drop the leading diagonal entry of each row)
-    std::vector<int64_t> rp(n + 1, 0);
-    std::vector<int32_t> c32;
-    std::vector<double2> v;
-    std::vector<double2> invd;
-    c32.reserve(F.nnz());
-    v.reserve(F.nnz());
-    if (upper) invd.resize(n);
+    T.B = B;
+    T.nblk = nblk;
+    T.rev = upper ? 1 : 0;
+    // strict entries of kernel row ip in ascending kernel column: for L the CSR row; for U
+    // the reversed strict part of row n-1-ip.
+    auto row_range = [&](int64_t ip, int64_t& q0, int64_t& q1) {
+        const int64_t i = upper ? n - 1 - ip : ip;
+        q0 = F.rowptr[i] + (upper ? 1 : 0);
+        q1 = F.rowptr[i + 1];
+    };
+    auto kcol = [&](int64_t q) -> int64_t { return upper ? n - 1 - F.col[q] : F.col[q]; };
+    auto entry = [&](int64_t q0, int64_t q1, int64_t t) -> int64_t { return upper ? q1 - 1 - t : q0 + t; };
+
+    // per row: far = columns < (k-2)B, near = (k-2)B <= column < kB, the rest is in-block
+    std::vector<int64_t> farptr(n + 1, 0), nrp(n + 1, 0);
+    std::vector<int64_t> cnt(n), ncnt(n);
+    parallel_for(n, threads, [&](int64_t lo, int64_t hi) {
+        for (int64_t ip = lo; ip < hi; ip++) {
+            int64_t q0, q1;
+            row_range(ip, q0, q1);
+            const int64_t kb = (ip / B) * B;
+            int64_t c = 0, nc = 0;
+            for (int64_t t = 0; t < q1 - q0; t++) {
+                const int64_t j = kcol(entry(q0, q1, t));
+                if (j >= kb) break;
+                if (j >= kb - 2 * B) nc++;
+                else c++;
+            }
+            cnt[ip] = c;
+            ncnt[ip] = nc;
+        }
+    });
     for (int64_t i = 0; i < n; i++) {
-        int64_t q0 = F.rowptr[i];
-        if (upper) {
-            const double2 u = F.val[q0];
-            const double d = u.x * u.x + u.y * u.y;
-            invd[i] = make_double2(u.x / d, -u.y / d);
-            q0++;
-        }
-        for (int64_t q = q0; q < F.rowptr[i + 1]; q++) {
-            c32.push_back((int32_t)F.col[q]);
-            v.push_back(F.val[q]);
-        }
-        rp[i + 1] = (int64_t)c32.size();
+        farptr[i + 1] = farptr[i] + cnt[i];
+        nrp[i + 1] = nrp[i] + ncnt[i];
     }
-    T.nnz = (int64_t)c32.size();
-    std::vector<int64_t> lev_ptr;
-    std::vector<int32_t> lev_rows;
-    levels(F.rowptr, F.col, n, upper, upper ? 1 : 0, lev_ptr, lev_rows);
-    T.nlev = (int64_t)lev_ptr.size() - 1;
-    SSB_CUDA(cudaMalloc(&T.rowptr, (n + 1) * sizeof(int64_t)));
-    SSB_CUDA(cudaMalloc(&T.col, std::max<int64_t>(1, T.nnz) * sizeof(int32_t)));
-    SSB_CUDA(cudaMalloc(&T.val, std::max<int64_t>(1, T.nnz) * sizeof(double2)));
-    SSB_CUDA(cudaMalloc(&T.lev_ptr, lev_ptr.size() * sizeof(int64_t)));
-    SSB_CUDA(cudaMalloc(&T.lev_rows, n * sizeof(int32_t)));
-    SSB_CUDA(cudaMemcpyAsync(T.rowptr, rp.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-    if (T.nnz) {
-        SSB_CUDA(cudaMemcpyAsync(T.col, c32.data(), T.nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-        SSB_CUDA(cudaMemcpyAsync(T.val, v.data(), T.nnz * sizeof(double2), cudaMemcpyHostToDevice, s));
+    const int64_t nf = farptr[n], nn = nrp[n];
+    T.nnz_far = nf;
+    T.nnz_near = nn;
+    T.nnz_strict = F.nnz() - (upper ? n : 0);
+
+    SSB_CUDA(cudaMalloc(&T.farptr, (n + 1) * sizeof(int64_t)));
+    SSB_CUDA(cudaMalloc(&T.nrp, (n + 1) * sizeof(int64_t)));
+    SSB_CUDA(cudaMalloc(&T.fcol, std::max<int64_t>(1, nf) * sizeof(int32_t)));
+    SSB_CUDA(cudaMalloc(&T.fval, std::max<int64_t>(1, nf) * sizeof(double2)));
+    SSB_CUDA(cudaMalloc(&T.ncol, std::max<int64_t>(1, nn) * sizeof(int32_t)));
+    SSB_CUDA(cudaMalloc(&T.nval, std::max<int64_t>(1, nn) * sizeof(double2)));
+    SSB_CUDA(cudaMalloc(&T.dinv, std::max<int64_t>(1, nblk * PK) * sizeof(double2)));
+    SSB_CUDA(cudaMalloc(&T.flags, std::max<int64_t>(1, nblk) * sizeof(uint32_t)));
+    SSB_CUDA(cudaMemsetAsync(T.flags, 0, std::max<int64_t>(1, nblk) * sizeof(uint32_t), s));
+    SSB_CUDA(cudaMemcpyAsync(T.farptr, farptr.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    SSB_CUDA(cudaMemcpyAsync(T.nrp, nrp.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    SSB_CUDA(cudaStreamSynchronize(s));
+
+    // entries, in row chunks of ~2^26 (bounded host staging)
+    const int64_t kChunk = (int64_t)1 << 26;
+    std::vector<int32_t> fc, nc;
+    std::vector<double2> fv, nv;
+    for (int64_t r0 = 0; r0 < n;) {
+        int64_t r1 = r0 + 1;
+        while (r1 < n && (farptr[r1 + 1] - farptr[r0]) + (nrp[r1 + 1] - nrp[r0]) <= kChunk) r1++;
+        const int64_t fb = farptr[r0], flen = farptr[r1] - fb;
+        const int64_t nb = nrp[r0], nlen = nrp[r1] - nb;
+        fc.resize(flen);
+        fv.resize(flen);
+        nc.resize(nlen);
+        nv.resize(nlen);
+        parallel_for(r1 - r0, threads, [&](int64_t lo, int64_t hi) {
+            for (int64_t ip = r0 + lo; ip < r0 + hi; ip++) {
+                int64_t q0, q1;
+                row_range(ip, q0, q1);
+                const int64_t of = farptr[ip] - fb, on = nrp[ip] - nb;
+                for (int64_t t = 0; t < cnt[ip]; t++) {
+                    const int64_t q = entry(q0, q1, t);
+                    fc[of + t] = (int32_t)kcol(q);
+                    fv[of + t] = F.val[q];
+                }
+                for (int64_t t = 0; t < ncnt[ip]; t++) {
+                    const int64_t q = entry(q0, q1, cnt[ip] + t);
+                    nc[on + t] = (int32_t)kcol(q);
+                    nv[on + t] = F.val[q];
+                }
+            }
+        });
+        if (flen) {
+            SSB_CUDA(cudaMemcpy(T.fcol + fb, fc.data(), flen * sizeof(int32_t), cudaMemcpyHostToDevice));
+            SSB_CUDA(cudaMemcpy(T.fval + fb, fv.data(), flen * sizeof(double2), cudaMemcpyHostToDevice));
+        }
+        if (nlen) {
+            SSB_CUDA(cudaMemcpy(T.ncol + nb, nc.data(), nlen * sizeof(int32_t), cudaMemcpyHostToDevice));
+            SSB_CUDA(cudaMemcpy(T.nval + nb, nv.data(), nlen * sizeof(double2), cudaMemcpyHostToDevice));
+        }
+        r0 = r1;
     }
-    SSB_CUDA(cudaMemcpyAsync(T.lev_ptr, lev_ptr.data(), lev_ptr.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-    SSB_CUDA(cudaMemcpyAsync(T.lev_rows, lev_rows.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-    if (upper) {
-        SSB_CUDA(cudaMalloc(&T.inv_diag, n * sizeof(double2)));
-        SSB_CUDA(cudaMemcpyAsync(T.inv_diag, invd.data(), n * sizeof(double2), cudaMemcpyHostToDevice, s));
+
+    // dense diagonal blocks -> explicit inverses, in block chunks
+    const int64_t kBlkChunk = std::max<int64_t>(1, ((int64_t)1 << 27) / (PK * 16));
+    std::vector<double2> ibuf;
+    for (int64_t k0 = 0; k0 < nblk; k0 += kBlkChunk) {
+        const int64_t k1 = std::min(nblk, k0 + kBlkChunk);
+        ibuf.assign((k1 - k0) * PK, make_double2(0.0, 0.0));
+        parallel_for(k1 - k0, threads, [&](int64_t lo, int64_t hi) {
+            std::vector<double2> D((size_t)B * B), X((size_t)B * B), inv(B);
+            for (int64_t k = k0 + lo; k < k0 + hi; k++) {
+                std::fill(D.begin(), D.end(), make_double2(0.0, 0.0));
+                const int64_t kb = k * B;
+                for (int r = 0; r < B; r++) {
+                    const int64_t ip = kb + r;
+                    if (ip >= n) {
+                        D[(size_t)r * B + r] = make_double2(1.0, 0.0);
+                        continue;
+                    }
+                    int64_t q0, q1;
+                    row_range(ip, q0, q1);
+                    for (int64_t t = cnt[ip] + ncnt[ip]; t < q1 - q0; t++) {
+                        const int64_t q = entry(q0, q1, t);
+                        D[(size_t)r * B + (kcol(q) - kb)] = F.val[q];
+                    }
+                    const int64_t i = upper ? n - 1 - ip : ip;
+                    D[(size_t)r * B + r] = upper ? F.val[F.rowptr[i]] : make_double2(1.0, 0.0);
+                }
+                for (int r = 0; r < B; r++) {
+                    const double2 d = D[(size_t)r * B + r];
+                    const double m = d.x * d.x + d.y * d.y;
+                    inv[r] = make_double2(d.x / m, -d.y / m);
+                }
+                // X = D^{-1}, column by column (forward substitution on unit vectors)
+                for (int j = 0; j < B; j++) {
+                    X[(size_t)j * B + j] = inv[j];
+                    for (int i = j + 1; i < B; i++) {
+                        double2 acc = make_double2(0.0, 0.0);
+                        for (int m = j; m < i; m++) acc = cadd(acc, cmul(D[(size_t)i * B + m], X[(size_t)m * B + j]));
+                        X[(size_t)i * B + j] = cmul(make_double2(-acc.x, -acc.y), inv[i]);
+                    }
+                }
+                double2* out = &ibuf[(size_t)(k - k0) * PK];
+                for (int j = 0; j < B; j++) {
+                    const int64_t cs = (int64_t)j * B - ((int64_t)j * (j - 1)) / 2;
+                    for (int i = j; i < B; i++) out[cs + (i - j)] = X[(size_t)i * B + j];
+                }
+            }
+        }, 4);
+        SSB_CUDA(cudaMemcpy(T.dinv + k0 * PK, ibuf.data(), (k1 - k0) * PK * sizeof(double2), cudaMemcpyHostToDevice));
     }
     SSB_CUDA(cudaStreamSynchronize(s));
+    block_trsv_prepare(T);
+}
+
+// Tuning knobs of the block substitution: rows per block and CTA size.
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
 }
 
 }  // namespace
@@ -177,8 +300,24 @@ void setup_problem(Problem& P, double drop_tol, double fill_factor, int threads,
     upload(A, P.A, s);
     if (!P.d_perm) SSB_CUDA(cudaMalloc(&P.d_perm, P.n * sizeof(int64_t)));
     SSB_CUDA(cudaMemcpyAsync(P.d_perm, P.perm.data(), P.n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-    upload_tri(P.hL, false, P.L, s);
-    upload_tri(P.hU, true, P.U, s);
+    if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+    const int B = env_int("SSB_TRSV_B", 128);
+    const int NT = env_int("SSB_TRSV_NT", B == 64 ? 256 : 512);
+    int64_t levL = 0, levU = 0;
+    std::thread lev([&] {
+        levL = count_levels(P.hL, false);
+        levU = count_levels(P.hU, true);
+    });
+    try {
+        build_block_tri(P.hL, false, B, NT, threads, P.L, s);
+        build_block_tri(P.hU, true, B, NT, threads, P.U, s);
+    } catch (...) {
+        lev.join();
+        throw;
+    }
+    lev.join();
+    P.L.nlev = levL;
+    P.U.nlev = levU;
     const double t3 = now_ms();
     P.have_setup = true;
     P.have_solution = false;
@@ -192,6 +331,8 @@ void setup_problem(Problem& P, double drop_tol, double fill_factor, int threads,
         info->levels_U = P.U.nlev;
         info->pivots_repaired = st.repaired;
         info->threads = st.threads;
+        info->trsv_block = B;
+        info->trsv_grid = P.L.grid;
         info->rcm_ms = t1 - t0;
         info->ilut_ms = t2 - t1;
         info->upload_ms = t3 - t2;

@@ -1,6 +1,6 @@
 """Probe one BASELINE config on the GPU: setup statistics, per-kernel times, a capped solve.
 
-usage: python scripts/probe.py NAME [max_iter]
+usage: python scripts/probe.py NAME [max_iter] [field=value ...]
 Prints one JSON line (setup_info, per-kernel device ms, solve_info).  Diagnostic only.
 """
 import json
@@ -31,13 +31,16 @@ def main():
     name = sys.argv[1]
     max_iter = int(sys.argv[2]) if len(sys.argv) > 2 else 100000
     p = CONFIGS[name]
+    for kv in sys.argv[3:]:
+        k, v = kv.split("=")
+        p = p.with_(**{k: type(getattr(p, k))(float(v)) if getattr(p, k) is not None else float(v)})
     st = torch.cuda.current_stream()
     t0 = time.perf_counter()
     s = pb.SteadyState(p, stream=st)
     t1 = time.perf_counter()
     s.setup()
     t2 = time.perf_counter()
-    out = {"name": name, "n": s.n, "build": s.build_info, "build_s": t1 - t0, "setup_s": t2 - t1,
+    out = {"name": name, "params": p.as_dict(), "n": s.n, "build": s.build_info, "build_s": t1 - t0, "setup_s": t2 - t1,
            "setup": s.setup_info}
     x = torch.randn(s.n, dtype=torch.complex128, device="cuda")
     out["ms"] = {"spmv": timed(lambda: s.spmv(x), st), "trsv_lower": timed(lambda: s.precond(x, 0), st, 2),
