@@ -134,7 +134,7 @@ def cpu_baseline(name: str, budget_s: float = 20.0):
     from oracle import liouvillian as lv
     from oracle import rcm as R
     from oracle import steadystate as ss
-    from oracle.ilut import ilut
+    from oracle.ilut import ilutp
     from oracle.trisolve import apply_preconditioner
     from oracle import gmres as G
 
@@ -142,7 +142,7 @@ def cpu_baseline(name: str, budget_s: float = 20.0):
     Lt, rhs, w, L = lv.constrained_system(p)
     perm = ss.order(Lt)
     A = R.permute(Lt, perm)
-    F = ilut(A, p.drop_tol, p.fill_factor)
+    F = ilutp(A, p.drop_tol, p.fill_factor, p.permtol)
     with threadpool_limits(limits=1):
         # calibrate: time a bounded number of Arnoldi steps (max_iter cap), one cycle at most
         t0 = time.perf_counter()
@@ -188,10 +188,12 @@ def workload_config(name, p, world):
             "l2": "flushed (256 MiB write) before every timed step, outside the step's events"}
 
 
-def tri_bytes(nnz, n, nlev, upper):
-    # strict entries (16 B value + 4 B column), row pointers, level schedule, b read, x written,
-    # x gathered once, (U) inverse diagonal
-    return nnz * 20 + (n + 1) * 8 + n * 4 + (nlev + 1) * 8 + 3 * n * 16 + (n * 16 if upper else 0)
+def precond_bytes(si, n):
+    """Algorithmic bytes of one M^{-1} application (both substitutions), DESIGN.md sec. 5:
+    every strict factor entry once (16 B value + 4 B column), U's diagonal, the row
+    pointers, and per factor the right-hand side read, x written and x read back once."""
+    strict = si["nnz_L"] + si["nnz_U"] - n
+    return strict * 20 + n * 16 + 2 * ((n + 1) * 8 + 3 * n * 16)
 
 
 def run_b200(args):
@@ -255,7 +257,9 @@ def run_b200(args):
     # --- kernel-level timing of the hot-path pieces on the same stream (roofline evidence)
     x = torch.randn(n, dtype=torch.complex128, device=dev)
     lvl = {}
-    for name, fn in (("trsv_lower", lambda: s.precond(x, 0)), ("trsv_upper", lambda: s.precond(x, 1)),
+    y = torch.empty_like(x)
+    for name, fn in (("trsv_lower", lambda: pb.ss_precond(s.handle, 0 | 4, x.data_ptr(), y.data_ptr())),
+                     ("trsv_upper", lambda: pb.ss_precond(s.handle, 1 | 4, x.data_ptr(), y.data_ptr())),
                      ("spmv", lambda: s.spmv(x))):
         fn()
         reps = 5
@@ -297,11 +301,10 @@ def run_b200(args):
         si = s.setup_info
         peak, peak_src = peaks()
         nlL, nlU = si["levels_L"], si["levels_U"]
-        bL = tri_bytes(si["nnz_L"] - 0, n, nlL, False)
-        bU = tri_bytes(si["nnz_U"] - n, n, nlU, True)
+        bytes_pc = precond_bytes(si, n)
         ms_pc = lvl["trsv_lower"] + lvl["trsv_upper"]
-        achieved = (bL + bU) / (ms_pc * 1e-3) / 1e9
-        tr = ncu_traffic("k_trsv_levels")
+        achieved = bytes_pc / (ms_pc * 1e-3) / 1e9
+        tr = ncu_traffic("k_chain_trsv")
         line = {
             "metric": METRIC, "value": it_sum / (ms_max * 1e-3), "unit": "iterations/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
@@ -312,11 +315,13 @@ def run_b200(args):
                        "fill": si["fill"], "nnz_L": si["nnz_L"], "nnz_U": si["nnz_U"],
                        "levels_L": nlL, "levels_U": nlU, "bandwidth_rcm": si["bandwidth_rcm"],
                        "time_to_steady_state_ms": ms_max / args.steps},
-            "roofline": {"bound": "hbm", "kernel": "k_trsv_levels (forward + backward substitution)",
+            "roofline": {"bound": "hbm", "kernel": "k_chain_trsv (L then U launch: one M^-1 application)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "peak_source": peak_src, "traffic": tr,
-                         "algorithmic_bytes_per_apply": bL + bU, "ms_per_apply": ms_pc,
-                         "kernel_ms": lvl},
+                         "algorithmic_bytes_per_apply": bytes_pc, "ms_per_apply": ms_pc,
+                         "kernel_ms": lvl, "trsv_block": si.get("trsv_block"),
+                         "trsv_q": [si.get("trsv_q_L"), si.get("trsv_q_U")],
+                         "note": "chain-latency bound: n/B dependent block steps per factor (DESIGN.md sec. 5)"},
             "e2e": {"value": e2e_it_sum / (e2e_max * 1e-3), "unit": "iterations/s",
                     "h2d_bytes_per_step": n * 16, "d2h_bytes_per_step": n * 16},
             "gpu_launches": int(launches),

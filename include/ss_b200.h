@@ -79,9 +79,13 @@ typedef struct ss_setup_info {
     int64_t levels_L;       /* dependency levels of the forward / backward substitutions    */
     int64_t levels_U;
     int32_t pivots_repaired;/* zero pivots replaced by tau_i (reading R6)                     */
+    int32_t pivot_swaps;    /* column exchanges made by the iLUTP pivoting (reading R13)      */
+    int32_t pad0;
     int32_t threads;        /* host threads used by the factorisation                        */
     int32_t trsv_block;     /* rows per block B of the block substitution (trsv.cu)          */
-    int32_t trsv_grid;      /* persistent CTAs of the block substitution (0 before first use) */
+    int32_t trsv_grid;      /* persistent CTAs of the block substitution (chain + helpers)   */
+    int32_t trsv_q_L;       /* smallest near window Q_k of the L / U substitution (source      */
+    int32_t trsv_q_U;       /*   blocks k-Q_k+1..k-1 on the chain SM, older ones on helpers)  */
     double rcm_ms, ilut_ms, upload_ms;
 } ss_setup_info;
 
@@ -101,12 +105,14 @@ typedef struct ss_solve_info {
  * on stream `cuda_stream` (a cudaStream_t, may be NULL).  *out receives a new handle. */
 int ss_build(const ss_params* p, void* cuda_stream, ss_problem** out, ss_build_info* info);
 
-/* One-time setup: RCM ordering of pattern(L~ + L~^T) (sec. III), the symmetric
- * permutation L~_RCM, the ILUT(drop_tol, fill_factor) factors (sec. II; rules
- * R4-R7 of DESIGN.md), their level schedules and the device layout of the hot
- * path.  n_threads <= 0 -> all host cores.  May be called again with other
- * drop_tol / fill_factor. */
-int ss_setup(ss_problem* h, double drop_tol, double fill_factor, int32_t n_threads,
+/* One-time setup: RCM ordering of pattern(L~ + L~^T) (sec. III), the
+ * symmetric permutation L~_RCM, the iLUTP(drop_tol, fill_factor, permtol) factors
+ * L~_RCM Pi ~ L U (sec. II, "dual-threshold and pivoting"; rules R4-R7, R13
+ * of DESIGN.md; permtol = 0: no column exchanges = plain ILUT), the block layout of the
+ * substitutions and its upload.  n_threads <= 0 -> all host cores.  May be called again
+ * with other parameters.  Errors: SS_ERR_ARG (negative parameter), SS_ERR_BREAKDOWN
+ * (zero pivot with drop_tol = 0). */
+int ss_setup(ss_problem* h, double drop_tol, double fill_factor, double permtol, int32_t n_threads,
              ss_setup_info* info);
 
 /* Solve Eq. (5) by left-preconditioned GMRES(restart) (Eq. (8)) from
@@ -144,6 +150,10 @@ int ss_export_matrix(const ss_problem* h, int32_t which, int64_t* rowptr, int64_
 /* Copy the RCM permutation perm[n] (new -> old: L~_RCM = L~[perm][:, perm]). */
 int ss_export_perm(const ss_problem* h, int64_t* perm);
 
+/* Copy the iLUTP column permutation colperm[n] (position -> column of L~_RCM:
+ * L~_RCM[:, colperm] ~ L U; the identity when no column was exchanged). */
+int ss_export_colperm(const ss_problem* h, int64_t* colperm);
+
 /* Copy an ILU factor to host CSR: which = 0: strict lower L (unit diagonal implicit),
  * rowptr[n+1], colidx[nnz_L], vals[2 nnz_L]; which = 1: U with its diagonal FIRST in
  * every row then strict upper columns ascending, rowptr[n+1], colidx[nnz_U], vals[2 nnz_U]. */
@@ -152,8 +162,12 @@ int ss_export_factors(const ss_problem* h, int32_t which, int64_t* rowptr, int64
 
 /* y = L~_RCM x  (device pointers, complex128 length n).                           */
 int ss_spmv(ss_problem* h, const void* x_dev, void* y_dev);
-/* y = L^{-1} x (which = 0), y = U^{-1} x (which = 1), y = U^{-1} L^{-1} x (which = 2);
- * device pointers, length n, x and y may not alias.                                */
+/* y = L^{-1} x (which = 0), y = Pi U^{-1} x (which = 1), y = M^{-1} x = Pi U^{-1} L^{-1} x
+ * (which = 2), Pi the iLUTP column permutation (ss_export_colperm);
+ * device pointers, length n, x and y may not alias.  which | SS_PRECOND_ASYNC: return
+ * right after the launches (stream-ordered, no host synchronisation; used to time the
+ * kernels with events).  which = 2 uses the handle's Krylov scratch vector.          */
+#define SS_PRECOND_ASYNC 4
 int ss_precond(ss_problem* h, int32_t which, const void* x_dev, void* y_dev);
 
 /* Diagnostic: run the block substitution of factor `which` (0 = L, 1 = U) on x_dev -> y_dev

@@ -36,6 +36,11 @@ def lib() -> ctypes.CDLL:
         L.oracle_ilut.argtypes = [ctypes.c_int64, P64, P64, PD, ctypes.c_double, ctypes.c_double,
                                   ctypes.POINTER(P64), ctypes.POINTER(P64), ctypes.POINTER(PD), P64,
                                   ctypes.POINTER(P64), ctypes.POINTER(P64), ctypes.POINTER(PD), P64]
+        L.oracle_ilutp.restype = ctypes.c_int
+        L.oracle_ilutp.argtypes = [ctypes.c_int64, P64, P64, PD, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                   ctypes.POINTER(P64), ctypes.POINTER(P64), ctypes.POINTER(PD), P64,
+                                   ctypes.POINTER(P64), ctypes.POINTER(P64), ctypes.POINTER(PD), P64,
+                                   ctypes.POINTER(P64)]
         L.oracle_rcm.restype = ctypes.c_int
         L.oracle_rcm.argtypes = [ctypes.c_int64, P64, P64, P64]
         L.oracle_free.restype = None

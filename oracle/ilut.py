@@ -32,6 +32,7 @@ class IluFactors:
     Up: np.ndarray   # upper triangular, diagonal FIRST in each row, then cols ascending
     Uj: np.ndarray
     Ux: np.ndarray
+    perm: np.ndarray | None = None   # ILUTP column permutation: A[:, perm] ~ L U (None: identity)
 
     @property
     def nnz(self) -> int:
@@ -83,6 +84,44 @@ def ilut(A, drop_tol: float, fill_factor: float) -> IluFactors:
     lp, lj, lx = take(Lp, Lj, Lx, Ln.value)
     up, uj, ux = take(Up, Uj, Ux, Un.value)
     return IluFactors(n, lp, lj, lx, up, uj, ux)
+
+
+def ilutp(A, drop_tol: float, fill_factor: float, permtol: float) -> IluFactors:
+    """ILUT with column pivoting ("iLUTP"; oracle_ilutp in ilut.c, reading R13):
+    A[:, perm] ~ L U.  permtol = 0 reproduces ilut() exactly (perm = identity)."""
+    A = sp.csr_matrix(A)
+    A.sort_indices()
+    n = A.shape[0]
+    rp = np.ascontiguousarray(A.indptr, dtype=np.int64)
+    ci = np.ascontiguousarray(A.indices, dtype=np.int64)
+    v = np.ascontiguousarray(A.data, dtype=np.complex128)
+    P64 = ctypes.POINTER(ctypes.c_int64)
+    PD = ctypes.POINTER(ctypes.c_double)
+    Lp, Lj, Up, Uj, Pm = P64(), P64(), P64(), P64(), P64()
+    Lx, Ux = PD(), PD()
+    Ln, Un = ctypes.c_int64(), ctypes.c_int64()
+    lib = _clib.lib()
+    rc = lib.oracle_ilutp(n, rp.ctypes.data_as(P64), ci.ctypes.data_as(P64), v.view(np.float64).ctypes.data_as(PD),
+                          float(drop_tol), float(fill_factor), float(permtol),
+                          ctypes.byref(Lp), ctypes.byref(Lj), ctypes.byref(Lx), ctypes.byref(Ln),
+                          ctypes.byref(Up), ctypes.byref(Uj), ctypes.byref(Ux), ctypes.byref(Un), ctypes.byref(Pm))
+    if rc != 0:
+        raise RuntimeError(f"oracle ILUTP failed (rc={rc}): zero pivot at row {-rc - 1}" if rc > -2000000000
+                           else "oracle ILUTP: out of memory")
+
+    def take(pp, jj, xx, nn):
+        p = np.ctypeslib.as_array(pp, (n + 1,)).copy()
+        j = np.ctypeslib.as_array(jj, (nn,)).copy() if nn else np.zeros(0, np.int64)
+        x = np.ctypeslib.as_array(xx, (2 * nn,)).copy().view(np.complex128) if nn else np.zeros(0, np.complex128)
+        for q in (pp, jj, xx):
+            lib.oracle_free(ctypes.cast(q, ctypes.c_void_p))
+        return p, j, x
+
+    lp, lj, lx = take(Lp, Lj, Lx, Ln.value)
+    up, uj, ux = take(Up, Uj, Ux, Un.value)
+    perm = np.ctypeslib.as_array(Pm, (n,)).copy()
+    lib.oracle_free(ctypes.cast(Pm, ctypes.c_void_p))
+    return IluFactors(n, lp, lj, lx, up, uj, ux, perm)
 
 
 def condest(F: IluFactors) -> float:

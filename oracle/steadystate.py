@@ -5,7 +5,7 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 Pipeline (sec. II-IV):
   build L~, rhs          Eq. (5)                         oracle.liouvillian
   RCM of L~ + L~^T       sec. III, PAPER.md:98            oracle.rcm / rcm_ref.c
-  ILUT of L~_RCM         sec. II, PAPER.md:94             oracle.ilut
+  iLUTP of L~_RCM        sec. II, PAPER.md:94             oracle.ilut (ilutp)
   GMRES(m), left prec.   sec. IV, Eq. (8)    oracle.gmres
   un-permute, unvec      Eq. (4) column stacking
 and the reference answer of the linear system itself:
@@ -30,7 +30,7 @@ import scipy.sparse.linalg as sla
 from . import liouvillian as lv
 from . import rcm as rcm_py
 from . import _clib
-from .ilut import ilut, IluFactors
+from .ilut import ilutp, IluFactors
 from .trisolve import apply_preconditioner
 from .gmres import gmres, GmresResult
 
@@ -83,7 +83,7 @@ def solve_iterative(p, use_c_rcm: bool = True) -> IterativeResult:
     perm = order(Lt, use_c=use_c_rcm)
     A = rcm_py.permute(Lt, perm)
     t2 = time.perf_counter()
-    F = ilut(A, p.drop_tol, p.fill_factor)
+    F = ilutp(A, p.drop_tol, p.fill_factor, p.permtol)
     t3 = time.perf_counter()
     res = gmres(lambda v: A @ v, lambda v: apply_preconditioner(F, v), rhs[perm], p.restart, p.tol,
                 p.max_iter)

@@ -43,10 +43,19 @@ def lower_unit_matrix(F) -> sp.csr_matrix:
     return sp.csr_matrix(F.L() + sp.identity(F.n, dtype=np.complex128, format="csr"))
 
 
+def unpivot(F, y: np.ndarray) -> np.ndarray:
+    """ILUTP: A Pi = L U, so M^{-1} = Pi U^{-1} L^{-1}: x[perm[p]] = y[p] (identity for ILUT)."""
+    if getattr(F, "perm", None) is None:
+        return y
+    x = np.empty_like(y)
+    x[F.perm] = y
+    return x
+
+
 def apply_preconditioner(F, v: np.ndarray, small_loops: bool = False) -> np.ndarray:
     if small_loops:
-        return backward(F, forward(F, v))
+        return unpivot(F, backward(F, forward(F, v)))
     Lm = lower_unit_matrix(F)
     Um = F.U()
     y = sla.spsolve_triangular(Lm, np.asarray(v, dtype=np.complex128), lower=True, unit_diagonal=True)
-    return sla.spsolve_triangular(Um, y, lower=False)
+    return unpivot(F, sla.spsolve_triangular(Um, y, lower=False))

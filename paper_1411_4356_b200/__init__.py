@@ -12,11 +12,11 @@ from __future__ import annotations
 
 from . import _lib
 from ._lib import (SSError, ss_build, ss_setup, ss_solve, ss_expect, ss_get_rho, ss_solve_host,
-                   ss_destroy, ss_sizes, ss_export_matrix, ss_export_perm, ss_export_factors, ss_spmv,
+                   ss_destroy, ss_sizes, ss_export_matrix, ss_export_perm, ss_export_colperm, ss_export_factors, ss_spmv,
                    ss_precond, ss_kernel_launches, ss_debug_trace_trsv)
 
 __all__ = ["SteadyState", "SSError", "ss_build", "ss_setup", "ss_solve", "ss_expect", "ss_get_rho",
-           "ss_solve_host", "ss_destroy", "ss_sizes", "ss_export_matrix", "ss_export_perm",
+           "ss_solve_host", "ss_destroy", "ss_sizes", "ss_export_matrix", "ss_export_perm", "ss_export_colperm",
            "ss_export_factors", "ss_spmv", "ss_precond", "ss_kernel_launches", "ss_debug_trace_trsv"]
 
 
@@ -40,10 +40,12 @@ class SteadyState:
         self.setup_info = None
         self.solve_info = None
 
-    def setup(self, drop_tol: float | None = None, fill_factor: float | None = None, threads: int = 0):
+    def setup(self, drop_tol: float | None = None, fill_factor: float | None = None,
+              permtol: float | None = None, threads: int = 0):
         p = self.params
         self.setup_info = ss_setup(self.handle, p.drop_tol if drop_tol is None else drop_tol,
-                                   p.fill_factor if fill_factor is None else fill_factor, threads)
+                                   p.fill_factor if fill_factor is None else fill_factor,
+                                   p.permtol if permtol is None else permtol, threads)
         return self
 
     def solve(self, restart: int | None = None, tol: float | None = None, max_iter: int | None = None):

@@ -42,8 +42,10 @@ class ss_setup_info(ctypes.Structure):
     _fields_ = [("nnz_L", ctypes.c_int64), ("nnz_U", ctypes.c_int64), ("fill", ctypes.c_double),
                 ("bandwidth_nat", ctypes.c_int64), ("bandwidth_rcm", ctypes.c_int64),
                 ("levels_L", ctypes.c_int64), ("levels_U", ctypes.c_int64),
-                ("pivots_repaired", ctypes.c_int32), ("threads", ctypes.c_int32),
+                ("pivots_repaired", ctypes.c_int32), ("pivot_swaps", ctypes.c_int32), ("pad0", ctypes.c_int32),
+                ("threads", ctypes.c_int32),
                 ("trsv_block", ctypes.c_int32), ("trsv_grid", ctypes.c_int32),
+                ("trsv_q_L", ctypes.c_int32), ("trsv_q_U", ctypes.c_int32),
                 ("rcm_ms", ctypes.c_double), ("ilut_ms", ctypes.c_double), ("upload_ms", ctypes.c_double)]
 
 
@@ -54,7 +56,7 @@ class ss_solve_info(ctypes.Structure):
 
 
 def struct_dict(s) -> dict:
-    return {k: getattr(s, k) for k, _ in s._fields_ if k != "pad"}
+    return {k: getattr(s, k) for k, _ in s._fields_ if not k.startswith("pad")}
 
 
 # (name, restype, argtypes) -- the exported symbols of include/ss_b200.h
@@ -64,7 +66,8 @@ PI64 = ctypes.POINTER(ctypes.c_int64)
 PD = ctypes.POINTER(ctypes.c_double)
 SIGNATURES = [
     ("ss_build", ctypes.c_int, [ctypes.POINTER(ss_params), P, ctypes.POINTER(P), ctypes.POINTER(ss_build_info)]),
-    ("ss_setup", ctypes.c_int, [P, D, D, I32, ctypes.POINTER(ss_setup_info)]),
+    ("ss_setup", ctypes.c_int, [P, D, D, D, I32, ctypes.POINTER(ss_setup_info)]),
+    ("ss_export_colperm", ctypes.c_int, [P, P]),
     ("ss_solve", ctypes.c_int, [P, I32, D, I32, ctypes.POINTER(ss_solve_info)]),
     ("ss_expect", ctypes.c_int, [P, PD, PD]),
     ("ss_get_rho", ctypes.c_int, [P, P, I32]),
@@ -120,10 +123,18 @@ def ss_build(p, stream: int = 0):
     return h, struct_dict(info)
 
 
-def ss_setup(h, drop_tol: float, fill_factor: float, n_threads: int = 0) -> dict:
+def ss_setup(h, drop_tol: float, fill_factor: float, permtol: float = 0.0, n_threads: int = 0) -> dict:
     info = ss_setup_info()
-    _check(load().ss_setup(h, float(drop_tol), float(fill_factor), int(n_threads), ctypes.byref(info)))
+    _check(load().ss_setup(h, float(drop_tol), float(fill_factor), float(permtol), int(n_threads),
+                           ctypes.byref(info)))
     return struct_dict(info)
+
+
+def ss_export_colperm(h) -> np.ndarray:
+    n = ss_sizes(h)["n"]
+    perm = np.empty(n, np.int64)
+    _check(load().ss_export_colperm(h, perm.ctypes.data))
+    return perm
 
 
 def ss_solve(h, restart: int, tol: float, max_iter: int) -> dict:

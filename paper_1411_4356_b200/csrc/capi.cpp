@@ -106,10 +106,11 @@ int ss_build(const ss_params* p, void* cuda_stream, ss_problem** out, ss_build_i
     SS_GUARD_END
 }
 
-int ss_setup(ss_problem* h, double drop_tol, double fill_factor, int32_t n_threads, ss_setup_info* info) {
+int ss_setup(ss_problem* h, double drop_tol, double fill_factor, double permtol, int32_t n_threads,
+             ss_setup_info* info) {
     SS_GUARD_BEGIN
     SSB_CHECK(h, SS_ERR_ARG, "ss_setup: NULL handle");
-    setup_problem(h->P, drop_tol, fill_factor, n_threads, info);
+    setup_problem(h->P, drop_tol, fill_factor, permtol, n_threads, info);
     SS_GUARD_END
 }
 
@@ -216,6 +217,14 @@ int ss_export_perm(const ss_problem* h, int64_t* perm) {
     SS_GUARD_END
 }
 
+int ss_export_colperm(const ss_problem* h, int64_t* colperm) {
+    SS_GUARD_BEGIN
+    SSB_CHECK(h && colperm, SS_ERR_ARG, "ss_export_colperm: NULL argument");
+    SSB_CHECK(h->P.have_setup, SS_ERR_STATE, "ss_export_colperm before ss_setup");
+    std::memcpy(colperm, h->P.colperm.data(), h->P.n * sizeof(int64_t));
+    SS_GUARD_END
+}
+
 int ss_export_factors(const ss_problem* h, int32_t which, int64_t* rowptr, int64_t* colidx, double* vals) {
     SS_GUARD_BEGIN
     SSB_CHECK(h && rowptr && colidx && vals, SS_ERR_ARG, "ss_export_factors: NULL argument");
@@ -240,6 +249,8 @@ int ss_spmv(ss_problem* h, const void* x_dev, void* y_dev) {
 int ss_precond(ss_problem* h, int32_t which, const void* x_dev, void* y_dev) {
     SS_GUARD_BEGIN
     SSB_CHECK(h && x_dev && y_dev && x_dev != y_dev, SS_ERR_ARG, "ss_precond: bad pointers");
+    const bool async = (which & SS_PRECOND_ASYNC) != 0;
+    which &= ~SS_PRECOND_ASYNC;
     SSB_CHECK(which >= 0 && which <= 2, SS_ERR_ARG, "ss_precond: which must be 0, 1 or 2");
     Problem& P = h->P;
     SSB_CHECK(P.have_setup, SS_ERR_STATE, "ss_precond before ss_setup");
@@ -250,14 +261,11 @@ int ss_precond(ss_problem* h, int32_t which, const void* x_dev, void* y_dev) {
     } else if (which == 1) {
         block_trsv(P.U, x, y, P.stream);
     } else {
-        double2* tmp = nullptr;
-        SSB_CUDA(cudaMalloc(&tmp, P.n * sizeof(double2)));
-        block_trsv(P.L, x, tmp, P.stream);
-        block_trsv(P.U, tmp, y, P.stream);
-        SSB_CUDA(cudaStreamSynchronize(P.stream));
-        cudaFree(tmp);
+        ensure_krylov(P, P.K.m > 0 ? P.K.m : 1);
+        block_trsv(P.L, x, P.K.t, P.stream);
+        block_trsv(P.U, P.K.t, y, P.stream);
     }
-    SSB_CUDA(cudaStreamSynchronize(P.stream));
+    if (!async) SSB_CUDA(cudaStreamSynchronize(P.stream));
     SS_GUARD_END
 }
 

@@ -45,44 +45,64 @@ struct HostCSR {
 };
 
 // Triangular factor on the device in the block layout of trsv.cu (kernel index space:
-// L as is, U reversed i' = n-1-i so that both are lower triangular).
+// L as is, U reversed i' = n-1-i so that both are lower triangular; blocks of B rows).
+// near entries per block staged in shared memory by trsv.cu (two stages must fit next to
+// the inverse blocks in 227 KB)
+constexpr int near_cap(int B) { return B <= 32 ? 4096 : 2560; }
+
 struct TriArgs {
     int64_t n, nblk;
     int32_t rev, B;
-    const int64_t* farptr;    // [n+1] entries of row i' with source block <= k-3 (k = i'/B)
+    const int64_t* farptr;    // [n+1] entries of row i' with source block <= k-Q (k = i'/B)
     const int32_t* fcol;      //       kernel-space columns, ascending within a row
     const double2* fval;
-    const int64_t* nrp;       // [n+1] entries of row i' with source block k-2 or k-1
-    const int32_t* ncol;
+    const int64_t* nbp;       // [nblk+1] start of block k's near list (multiple of 4 entries)
+    const int32_t* ncol;      //       near entries (source blocks k-Q+1 .. k-1), rows in order
     const double2* nval;
+    const int32_t* nloc;      // [nblk][B+4] row pointers of the near list, relative to nbp[k]
     const double2* dinv;      // [nblk][B(B+1)/2] inverse diagonal blocks, packed lower, column-major
-    uint32_t* flags;          // [nblk] completion flags (value = launch epoch)
+    double2* rfar;            // [nblk*B] b - (far part), written by the helper CTAs
+    const int64_t* operm;     // [n] output permutation out[operm[i]] = x[i] (ILUTP columns), or null
+    uint32_t* fflag;          // [nblk] "rfar of block k is ready" (value = launch epoch)
+    unsigned long long* xfront;   // (epoch << 32) | number of blocks of x published
 };
 
 struct DevBlockTri {
     int64_t n = 0, nblk = 0, nnz_far = 0, nnz_near = 0, nnz_strict = 0;
-    int B = 0, rev = 0, nt = 0;   // rows per block, reversed (U), threads per CTA
+    int B = 0, rev = 0, nt = 0, Q = 0;   // rows per block, reversed (U), threads per CTA, near window
     int64_t* farptr = nullptr;
     int32_t* fcol = nullptr;
     double2* fval = nullptr;
-    int64_t* nrp = nullptr;
+    int64_t* nbp = nullptr;
     int32_t* ncol = nullptr;
     double2* nval = nullptr;
+    int32_t* nloc = nullptr;
     double2* dinv = nullptr;
-    uint32_t* flags = nullptr;
+    double2* rfar = nullptr;
+    uint32_t* fflag = nullptr;
+    unsigned long long* xfront = nullptr;
+    int64_t* operm = nullptr;   // U of ILUTP: out[operm[p]] = x[p] (column permutation), else null
+    double2* xwork = nullptr;   // position-space x when operm is set
     uint32_t epoch = 0;
     int grid = 0;
     int64_t nlev = 0;   // row-level dependency levels (diagnostic)
-    TriArgs args() const { return TriArgs{n, nblk, rev, B, farptr, fcol, fval, nrp, ncol, nval, dinv, flags}; }
+    TriArgs args() const {
+        return TriArgs{n, nblk, rev, B, farptr, fcol, fval, nbp, ncol, nval, nloc, dinv, rfar, operm, fflag, xfront};
+    }
     void release() {
         cudaFree(farptr);
         cudaFree(fcol);
         cudaFree(fval);
-        cudaFree(nrp);
+        cudaFree(nbp);
         cudaFree(ncol);
         cudaFree(nval);
+        cudaFree(nloc);
         cudaFree(dinv);
-        cudaFree(flags);
+        cudaFree(rfar);
+        cudaFree(fflag);
+        cudaFree(xfront);
+        cudaFree(operm);
+        cudaFree(xwork);
         *this = DevBlockTri();
     }
 };
@@ -131,6 +151,7 @@ struct Problem {
     bool have_setup = false;
 
     HostCSR hL, hU;             // host copies of the factors (export / tests)
+    std::vector<int64_t> colperm;   // ILUTP column permutation (position -> column of L~_RCM)
     DevBlockTri L, U;
     int64_t bw_nat = 0, bw_rcm = 0;
 
@@ -146,16 +167,19 @@ struct Problem {
 // build.cu
 void build_liouvillian(Problem& P);
 // setup.cpp
-void setup_problem(Problem& P, double drop_tol, double fill_factor, int threads, ss_setup_info* info);
+void setup_problem(Problem& P, double drop_tol, double fill_factor, double permtol, int threads,
+                   ss_setup_info* info);
 // rcm.cpp
 std::vector<int64_t> rcm_order(int64_t n, const std::vector<int64_t>& rowptr, const std::vector<int64_t>& col);
 // ilut.cpp
 struct IlutStats {
     int32_t repaired = 0;
+    int32_t swaps = 0;
     int32_t threads = 1;
 };
-void ilut_factor(const HostCSR& A, double drop_tol, double fill_factor, int threads, HostCSR& L,
-                 HostCSR& U, IlutStats& st);
+// ILUTP: A[:, colperm] ~ L U (L strict lower, unit diagonal implicit; U diagonal first)
+void ilut_factor(const HostCSR& A, double drop_tol, double fill_factor, double permtol, int threads, HostCSR& L,
+                 HostCSR& U, std::vector<int64_t>& colperm, IlutStats& st);
 // spmv.cu
 void spmv(const DevCSR& A, const double2* x, double2* y, cudaStream_t s);
 // trsv.cu: x = T^{-1} b for one factor (b, x in natural index order; x must not alias b)

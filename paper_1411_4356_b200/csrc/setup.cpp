@@ -115,14 +115,15 @@ int64_t count_levels(const HostCSR& F, bool upper) {
 
 // Block layout of one ILU factor for trsv.cu.  Kernel index space: L as is; U reversed
 // (i' = n-1-i), which turns the upper factor into a lower one.  Row i' of block k splits
-// its strict entries (ascending kernel column) into "far" (column < (k-2)B), "near"
-// ((k-2)B <= column < kB) and in-block; far and near go to two CSR arrays, the in-block
-// entries and the diagonal (1 for L, u_ii for U) form the dense block D_k, whose
-// inverse is stored packed (lower, column-major; column j = rows j..B-1).  The last
-// block is padded with identity rows.
-void build_block_tri(const HostCSR& F, bool upper, int B, int nt, int threads, DevBlockTri& T, cudaStream_t s) {
+// its strict entries (ascending kernel column) into "far" (source block <= k-Q), "near"
+// (source blocks k-Q+1 .. k-1) and in-block.  Far entries form a CSR; the near entries
+// of a block form one list (rows in order, start padded to 4 entries for TMA, row
+// pointers relative to the block start); the in-block entries and the diagonal (1 for
+// L, u_ii for U) form the dense block D_k, whose inverse is stored packed (lower,
+// column-major; column j = rows j..B-1).  The last block is padded with identity rows.
+void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads, DevBlockTri& T,
+                     cudaStream_t s) {
     T.release();
-    T.nt = nt;
     const int64_t n = F.n;
     const int64_t nblk = (n + B - 1) / B;
     const int64_t PK = (int64_t)block_trsv_packed(B);
@@ -140,65 +141,115 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int nt, int threads, D
     auto kcol = [&](int64_t q) -> int64_t { return upper ? n - 1 - F.col[q] : F.col[q]; };
     auto entry = [&](int64_t q0, int64_t q1, int64_t t) -> int64_t { return upper ? q1 - 1 - t : q0 + t; };
 
-    // per row: far = columns < (k-2)B, near = (k-2)B <= column < kB, the rest is in-block
-    std::vector<int64_t> farptr(n + 1, 0), nrp(n + 1, 0);
-    std::vector<int64_t> cnt(n), ncnt(n);
+    // per row: entries per source distance d = k - source block (d = 1 .. kMaxQ-1; d >= kMaxQ
+    // counted together); the near window Q (near = d < Q, far = d >= Q) is the largest
+    // Q <= Qmax whose per-block near lists fit the shared-memory stage (kNearCap)
+    constexpr int kMaxQ = 8;
+    std::vector<int64_t> dcnt((size_t)n * kMaxQ, 0);   // [row][d], d = 0 means ">= kMaxQ"
+    std::vector<int64_t> nin(n);                        // strict entries left of the block
     parallel_for(n, threads, [&](int64_t lo, int64_t hi) {
         for (int64_t ip = lo; ip < hi; ip++) {
             int64_t q0, q1;
             row_range(ip, q0, q1);
-            const int64_t kb = (ip / B) * B;
-            int64_t c = 0, nc = 0;
+            const int64_t k = ip / B, kb = k * B;
+            int64_t c = 0;
             for (int64_t t = 0; t < q1 - q0; t++) {
                 const int64_t j = kcol(entry(q0, q1, t));
                 if (j >= kb) break;
-                if (j >= kb - 2 * B) nc++;
-                else c++;
+                const int64_t d = k - j / B;
+                dcnt[(size_t)ip * kMaxQ + (d < kMaxQ ? d : 0)]++;
+                c++;
             }
-            cnt[ip] = c;
-            ncnt[ip] = nc;
+            nin[ip] = c;
         }
     });
-    for (int64_t i = 0; i < n; i++) {
-        farptr[i + 1] = farptr[i] + cnt[i];
-        nrp[i + 1] = nrp[i] + ncnt[i];
+    // per block: the largest window Q_k <= Qmax whose near list fits the stage (Q_k = 1:
+    // no near entries -- every source is then streamed by the helpers, still exact)
+    const int qmax = std::max(1, std::min(kMaxQ, q_max));
+    std::vector<int> qk(nblk, qmax);
+    int qmin = qmax;
+    parallel_for(nblk, threads, [&](int64_t lo, int64_t hi) {
+        for (int64_t k = lo; k < hi; k++) {
+            int q = qmax;
+            for (; q > 1; q--) {
+                int64_t c = 0;
+                for (int64_t ip = k * B; ip < std::min(n, (k + 1) * B); ip++)
+                    for (int d = 1; d < q; d++) c += dcnt[(size_t)ip * kMaxQ + d];
+                if (c <= near_cap(B)) break;
+            }
+            qk[k] = q;
+        }
+    }, 16);
+    for (int64_t k = 0; k < nblk; k++) qmin = std::min(qmin, qk[k]);
+    T.Q = qmin;
+    std::vector<int64_t> cnt(n), ncnt(n);   // far / near entries per row
+    for (int64_t ip = 0; ip < n; ip++) {
+        int64_t nc = 0;
+        for (int d = 1; d < qk[ip / B]; d++) nc += dcnt[(size_t)ip * kMaxQ + d];
+        ncnt[ip] = nc;
+        cnt[ip] = nin[ip] - nc;
     }
-    const int64_t nf = farptr[n], nn = nrp[n];
+    std::vector<int64_t>().swap(dcnt);
+    std::vector<int64_t> farptr(n + 1, 0), nbp(nblk + 1, 0), nrow(n + 1, 0);   // nrow: global near row starts
+    std::vector<int32_t> nloc((size_t)nblk * (B + 4), 0);
+    for (int64_t i = 0; i < n; i++) farptr[i + 1] = farptr[i] + cnt[i];
+    for (int64_t k = 0; k < nblk; k++) {
+        int64_t off = 0;
+        for (int r = 0; r < B; r++) {
+            const int64_t ip = k * B + r;
+            nloc[(size_t)k * (B + 4) + r] = (int32_t)off;
+            if (ip < n) {
+                nrow[ip] = nbp[k] + off;
+                off += ncnt[ip];
+            }
+        }
+        for (int r = B; r < B + 4; r++) nloc[(size_t)k * (B + 4) + r] = (int32_t)off;
+        nbp[k + 1] = nbp[k] + ((off + 3) & ~(int64_t)3);
+    }
+    const int64_t nf = farptr[n], nn = nbp[nblk];
     T.nnz_far = nf;
-    T.nnz_near = nn;
+    T.nnz_near = 0;
+    for (int64_t i = 0; i < n; i++) T.nnz_near += ncnt[i];
     T.nnz_strict = F.nnz() - (upper ? n : 0);
 
     SSB_CUDA(cudaMalloc(&T.farptr, (n + 1) * sizeof(int64_t)));
-    SSB_CUDA(cudaMalloc(&T.nrp, (n + 1) * sizeof(int64_t)));
     SSB_CUDA(cudaMalloc(&T.fcol, std::max<int64_t>(1, nf) * sizeof(int32_t)));
     SSB_CUDA(cudaMalloc(&T.fval, std::max<int64_t>(1, nf) * sizeof(double2)));
-    SSB_CUDA(cudaMalloc(&T.ncol, std::max<int64_t>(1, nn) * sizeof(int32_t)));
-    SSB_CUDA(cudaMalloc(&T.nval, std::max<int64_t>(1, nn) * sizeof(double2)));
+    SSB_CUDA(cudaMalloc(&T.nbp, (nblk + 1) * sizeof(int64_t)));
+    SSB_CUDA(cudaMalloc(&T.ncol, std::max<int64_t>(4, nn) * sizeof(int32_t)));
+    SSB_CUDA(cudaMalloc(&T.nval, std::max<int64_t>(4, nn) * sizeof(double2)));
+    SSB_CUDA(cudaMalloc(&T.nloc, nloc.size() * sizeof(int32_t)));
     SSB_CUDA(cudaMalloc(&T.dinv, std::max<int64_t>(1, nblk * PK) * sizeof(double2)));
-    SSB_CUDA(cudaMalloc(&T.flags, std::max<int64_t>(1, nblk) * sizeof(uint32_t)));
-    SSB_CUDA(cudaMemsetAsync(T.flags, 0, std::max<int64_t>(1, nblk) * sizeof(uint32_t), s));
+    SSB_CUDA(cudaMalloc(&T.rfar, std::max<int64_t>(1, nblk * B) * sizeof(double2)));
+    SSB_CUDA(cudaMalloc(&T.fflag, std::max<int64_t>(1, nblk) * sizeof(uint32_t)));
+    SSB_CUDA(cudaMalloc(&T.xfront, sizeof(unsigned long long)));
+    SSB_CUDA(cudaMemsetAsync(T.fflag, 0, std::max<int64_t>(1, nblk) * sizeof(uint32_t), s));
+    SSB_CUDA(cudaMemsetAsync(T.xfront, 0, sizeof(unsigned long long), s));
+    SSB_CUDA(cudaMemsetAsync(T.ncol, 0, std::max<int64_t>(4, nn) * sizeof(int32_t), s));   // padding entries
     SSB_CUDA(cudaMemcpyAsync(T.farptr, farptr.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-    SSB_CUDA(cudaMemcpyAsync(T.nrp, nrp.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    SSB_CUDA(cudaMemcpyAsync(T.nbp, nbp.data(), (nblk + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    SSB_CUDA(cudaMemcpyAsync(T.nloc, nloc.data(), nloc.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     SSB_CUDA(cudaStreamSynchronize(s));
 
-    // entries, in row chunks of ~2^26 (bounded host staging)
+    // entries, in row chunks of ~2^26 (bounded host staging); near rows of a block are
+    // contiguous from nbp[k], so a row chunk maps to one contiguous near range too
     const int64_t kChunk = (int64_t)1 << 26;
     std::vector<int32_t> fc, nc;
     std::vector<double2> fv, nv;
     for (int64_t r0 = 0; r0 < n;) {
         int64_t r1 = r0 + 1;
-        while (r1 < n && (farptr[r1 + 1] - farptr[r0]) + (nrp[r1 + 1] - nrp[r0]) <= kChunk) r1++;
+        while (r1 < n && (farptr[r1 + 1] - farptr[r0]) + (nrow[r1] + ncnt[r1] - nrow[r0]) <= kChunk) r1++;
         const int64_t fb = farptr[r0], flen = farptr[r1] - fb;
-        const int64_t nb = nrp[r0], nlen = nrp[r1] - nb;
+        const int64_t nb = nrow[r0], nlen = nrow[r1 - 1] + ncnt[r1 - 1] - nb;
         fc.resize(flen);
         fv.resize(flen);
-        nc.resize(nlen);
-        nv.resize(nlen);
+        nc.assign(nlen, 0);
+        nv.assign(nlen, make_double2(0.0, 0.0));
         parallel_for(r1 - r0, threads, [&](int64_t lo, int64_t hi) {
             for (int64_t ip = r0 + lo; ip < r0 + hi; ip++) {
                 int64_t q0, q1;
                 row_range(ip, q0, q1);
-                const int64_t of = farptr[ip] - fb, on = nrp[ip] - nb;
+                const int64_t of = farptr[ip] - fb, on = nrow[ip] - nb;
                 for (int64_t t = 0; t < cnt[ip]; t++) {
                     const int64_t q = entry(q0, q1, t);
                     fc[of + t] = (int32_t)kcol(q);
@@ -215,7 +266,7 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int nt, int threads, D
             SSB_CUDA(cudaMemcpy(T.fcol + fb, fc.data(), flen * sizeof(int32_t), cudaMemcpyHostToDevice));
             SSB_CUDA(cudaMemcpy(T.fval + fb, fv.data(), flen * sizeof(double2), cudaMemcpyHostToDevice));
         }
-        if (nlen) {
+        if (nlen > 0) {
             SSB_CUDA(cudaMemcpy(T.ncol + nb, nc.data(), nlen * sizeof(int32_t), cudaMemcpyHostToDevice));
             SSB_CUDA(cudaMemcpy(T.nval + nb, nv.data(), nlen * sizeof(double2), cudaMemcpyHostToDevice));
         }
@@ -283,7 +334,8 @@ int env_int(const char* name, int dflt) {
 
 }  // namespace
 
-void setup_problem(Problem& P, double drop_tol, double fill_factor, int threads, ss_setup_info* info) {
+void setup_problem(Problem& P, double drop_tol, double fill_factor, double permtol, int threads,
+                   ss_setup_info* info) {
     cudaStream_t s = P.stream;
     P.have_setup = false;
     const double t0 = now_ms();
@@ -295,22 +347,29 @@ void setup_problem(Problem& P, double drop_tol, double fill_factor, int threads,
     P.bw_rcm = bandwidth(A);
     const double t1 = now_ms();
     IlutStats st;
-    ilut_factor(A, drop_tol, fill_factor, threads, P.hL, P.hU, st);
+    ilut_factor(A, drop_tol, fill_factor, permtol, threads, P.hL, P.hU, P.colperm, st);
     const double t2 = now_ms();
     upload(A, P.A, s);
     if (!P.d_perm) SSB_CUDA(cudaMalloc(&P.d_perm, P.n * sizeof(int64_t)));
     SSB_CUDA(cudaMemcpyAsync(P.d_perm, P.perm.data(), P.n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
     if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
-    const int B = env_int("SSB_TRSV_B", 128);
-    const int NT = env_int("SSB_TRSV_NT", B == 64 ? 256 : 512);
+    const int B = env_int("SSB_TRSV_B", 32);
+    const int QMAX = env_int("SSB_TRSV_Q", 8);
     int64_t levL = 0, levU = 0;
     std::thread lev([&] {
         levL = count_levels(P.hL, false);
         levU = count_levels(P.hU, true);
     });
     try {
-        build_block_tri(P.hL, false, B, NT, threads, P.L, s);
-        build_block_tri(P.hU, true, B, NT, threads, P.U, s);
+        build_block_tri(P.hL, false, B, QMAX, threads, P.L, s);
+        build_block_tri(P.hU, true, B, QMAX, threads, P.U, s);
+        bool identity = true;
+        for (int64_t q = 0; q < P.n && identity; q++) identity = P.colperm[q] == q;
+        if (!identity) {   // ILUTP exchanged columns: the U substitution scatters x = Pi y
+            SSB_CUDA(cudaMalloc(&P.U.operm, P.n * sizeof(int64_t)));
+            SSB_CUDA(cudaMalloc(&P.U.xwork, P.n * sizeof(double2)));
+            SSB_CUDA(cudaMemcpy(P.U.operm, P.colperm.data(), P.n * sizeof(int64_t), cudaMemcpyHostToDevice));
+        }
     } catch (...) {
         lev.join();
         throw;
@@ -330,9 +389,12 @@ void setup_problem(Problem& P, double drop_tol, double fill_factor, int threads,
         info->levels_L = P.L.nlev;
         info->levels_U = P.U.nlev;
         info->pivots_repaired = st.repaired;
+        info->pivot_swaps = st.swaps;
         info->threads = st.threads;
         info->trsv_block = B;
         info->trsv_grid = P.L.grid;
+        info->trsv_q_L = P.L.Q;
+        info->trsv_q_U = P.U.Q;
         info->rcm_ms = t1 - t0;
         info->ilut_ms = t2 - t1;
         info->upload_ms = t3 - t2;

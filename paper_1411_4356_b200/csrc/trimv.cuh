@@ -22,7 +22,7 @@ struct Tiles {
     static constexpr int kRowBlocks = B / 32;
     static constexpr int kSegs = B / CW;
     // tiles of row block a: segments s with s*CW <= 32a + 31
-    static constexpr int segs_of(int a) { return (32 * a + 31) / CW + 1; }
+    __host__ __device__ static constexpr int segs_of(int a) { return (32 * a + 31) / CW + 1; }
     static constexpr int count() {
         int c = 0;
         for (int a = 0; a < kRowBlocks; a++) c += segs_of(a);
@@ -45,6 +45,16 @@ struct Tiles {
     }
 };
 
+// Shared-memory load that ptxas may not sink next to its use (asm volatile keeps the
+// batch of loads together at the head of the group).
+__device__ __forceinline__ double2 lds2(const double2* p) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "r"((uint32_t)__cvta_generic_to_shared(p)));
+    return v;
+}
+
 __device__ __forceinline__ double2 cfma2(double2 acc, double2 a, double2 b) {
     acc.x = fma(a.x, b.x, acc.x);
     acc.x = fma(-a.y, b.y, acc.x);
@@ -53,45 +63,61 @@ __device__ __forceinline__ double2 cfma2(double2 acc, double2 a, double2 b) {
     return acc;
 }
 
-// One tile: rows 32A + lane, columns CW*S .. CW*S + CW-1 (j <= i only).
-template <int B, int CW, int A, int S>
-__device__ __forceinline__ void tile(const double2* __restrict__ sInv, const double2* __restrict__ sR,
-                                     double2* __restrict__ sPart, int lane) {
+// One tile, generic in (A, S) so that every warp runs the same code (I-cache friendly):
+// rows i = 32A + lane, columns j0 .. j0+CW-1 (j0 = CW*S).  Entry (i, j0+jj) sits at
+// p + jj*st - jj(jj-1)/2 with p = &(i, j0) and st = B - j0 - 1, so each column costs one
+// IMAD.  Loads are issued 8 columns ahead of their FMAs (asm volatile keeps them
+// batched), and a diagonal tile zeroes its j > i terms by select (those reads land in
+// the tail of column j-1, inside the array).
+template <int B, int CW>
+__device__ __forceinline__ void tile(int A, int S, const double2* __restrict__ sInv,
+                                     const double2* __restrict__ sR, double2* __restrict__ sPart, int lane) {
     const int i = 32 * A + lane;
-    const double2* base = sInv + i;   // + cs(j) - j
+    const int j0 = CW * S;
+    const double2* p = sInv + (j0 * B - (j0 * (j0 - 1)) / 2 - j0 + i);
+    const double2* r = sR + j0;
+    const int st = B - j0 - 1;
+    const bool diag = j0 + CW - 1 > 32 * A;
     double2 acc[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0),
                       make_double2(0.0, 0.0)};
 #pragma unroll
-    for (int jj = 0; jj < CW; jj++) {
-        const int j = CW * S + jj;
-        const int off = j * B - (j * (j - 1)) / 2 - j;
-        if (CW * S + CW - 1 <= 32 * A || j <= i) acc[jj & 3] = cfma2(acc[jj & 3], base[off], sR[j]);
-    }
-    const double2 s = make_double2((acc[0].x + acc[1].x) + (acc[2].x + acc[3].x),
-                                   (acc[0].y + acc[1].y) + (acc[2].y + acc[3].y));
-    sPart[S * B + i] = s;
-}
-
-template <int B, int CW, int T>
-__device__ __forceinline__ void dispatch(int t, const double2* sInv, const double2* sR, double2* sPart, int lane) {
-    using TL = Tiles<B, CW>;
-    if constexpr (T < TL::kCount) {
-        if (t == T) {
-            tile<B, CW, TL::row_block(T), TL::seg(T)>(sInv, sR, sPart, lane);
-            return;
+    for (int g = 0; g < CW; g += 8) {
+        double2 m[8], rv[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const int jj = g + u;
+            m[u] = lds2(p + (jj * st - (jj * (jj - 1)) / 2));
+            rv[u] = lds2(r + jj);
         }
-        dispatch<B, CW, T + 1>(t, sInv, sR, sPart, lane);
+        if (diag) {
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const bool off = j0 + g + u > i;
+                m[u].x = off ? 0.0 : m[u].x;
+                m[u].y = off ? 0.0 : m[u].y;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) acc[u & 3] = cfma2(acc[u & 3], m[u], rv[u]);
     }
+    sPart[S * B + i] = make_double2((acc[0].x + acc[1].x) + (acc[2].x + acc[3].x),
+                                    (acc[0].y + acc[1].y) + (acc[2].y + acc[3].y));
 }
 
-// Whole CTA (NT threads): sPart[s*B + i] = sum over the tile (row block of i, segment s).
-// The caller synchronises, then sums with sum_row().
-template <int B, int NT, int CW>
-__device__ __forceinline__ void matvec_tiles(const double2* sInv, const double2* sR, double2* sPart) {
+// All tiles of the lower triangle, dealt round-robin to the warps w0 .. w0+NW-1 of the
+// calling group (warp-uniform).  The caller synchronises, then sums with sum_row().
+template <int B, int CW, int NW>
+__device__ __forceinline__ void matvec_tiles(const double2* sInv, const double2* sR, double2* sPart, int warp,
+                                             int lane) {
     using TL = Tiles<B, CW>;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr int NW = NT / 32;
-    for (int t = warp; t < TL::kCount; t += NW) dispatch<B, CW, 0>(t, sInv, sR, sPart, lane);
+    for (int t = warp; t < TL::kCount; t += NW) {
+        int a = 0, s = t;
+        while (s >= TL::segs_of(a)) {
+            s -= TL::segs_of(a);
+            a++;
+        }
+        tile<B, CW>(a, s, sInv, sR, sPart, lane);
+    }
 }
 
 // x_i = sum over the segments that row i's tiles cover, in segment order.

@@ -1,10 +1,10 @@
 """Critical-path breakdown of the block substitution (trsv.cu) from %globaltimer stamps
-(per block: start, warp-0 far done, all far done, near done, x stored, flag released).
+(per block: chain data ready, near done, mat-vec done, x stored; helper far published;
+producer saw the flag; frontier published; helper start).
 
 usage: python scripts/trace_trsv.py NAME [field=value ...]
-For each factor prints medians (ns) of: step (flag k-1 -> flag k), frontier latency
-(flag k-1 released -> CTA of block k sees it), near part, mat-vec + store, release,
-and the slack of the far part (far done - flag k-1 released; negative = early).
+For each factor prints medians (ns) of the chain step and its parts, and how far the
+helpers run ahead of the chain.
 """
 import json
 import os
@@ -34,23 +34,23 @@ def main():
         tr = tr - t0
         rel = tr[1:, :]
         prev = tr[:-1, 5]
-        stored_prev = tr[:-1, 4]
+        done_prev = tr[:-1, 3]
+        med = lambda v: float(np.median(v))
         d = {
             "blocks": int(tr.shape[0]),
-            "total_us": float(tr[:, 5].max() / 1e3),
-            "step_ns": float(np.median(tr[1:, 4] - tr[:-1, 4])),
-            "far_barrier_minus_prev_store_ns": float(np.median(rel[:, 2] - stored_prev)),
-            "near_done_minus_prev_store_ns": float(np.median(rel[:, 3] - stored_prev)),
-            "near_ns": float(np.median(rel[:, 3] - rel[:, 2])),
-            "matvec_store_ns": float(np.median(rel[:, 4] - rel[:, 3])),
-            "inverse_wait_ns": float(np.median(rel[:, 6] - rel[:, 3])),
-            "matvec_ns": float(np.median(rel[:, 7] - rel[:, 6])),
-            "store_ns": float(np.median(rel[:, 4] - rel[:, 7])),
-            "release_ns": float(np.median(rel[:, 5] - rel[:, 4])),
-            "x_staged_minus_prev_store_ns": float(np.median(rel[:, 1] - stored_prev)),
-            "near_done_minus_x_staged_ns": float(np.median(rel[:, 3] - rel[:, 1])),
-            "far_late_frac": float(np.mean(rel[:, 2] > stored_prev)),
-            "first_blocks": tr[:4].tolist(),
+            "total_us": float(tr[:, 3].max() / 1e3),
+            "step_ns": med(tr[1:, 3] - tr[:-1, 3]),
+            "chain_wait_ns": med(rel[:, 0] - done_prev),
+            "near_ns": med(rel[:, 1] - rel[:, 0]),
+            "matvec_ns": med(rel[:, 2] - rel[:, 1]),
+            "store_ns": med(rel[:, 3] - rel[:, 2]),
+            "helper_publish_minus_prev_done_ns": med(rel[:, 4] - done_prev),
+            "producer_sees_flag_after_publish_ns": med(tr[:, 5] - tr[:, 4]),
+            "near_loop_tid0_ns": med(tr[:, 6] - tr[:, 0]),
+            "near_shfl_tid0_ns": med(tr[:, 7] - tr[:, 6]),
+            "near_barrier_ns": med(tr[:, 1] - tr[:, 7]),
+            "chain_waited_on_helpers_frac": float(np.mean(rel[:, 5] > done_prev)),
+            "first_blocks": tr[:3].tolist(),
         }
         out[nm] = d
     print(json.dumps(out), flush=True)

@@ -28,9 +28,9 @@ __global__ void k_matvec(double2* out, long long* cyc, int reps) {
     long long t0 = clock64();
     for (int rep = 0; rep < reps; rep++) {
         if (MODE == 4) {
-        } else if (MODE == 6 || MODE == 7) {
-            constexpr int CW = MODE == 6 ? 16 : 32;
-            ssb::trimv::matvec_tiles<B, NT, CW>(sInv, sR, sPart);
+        } else if (MODE == 6 || MODE == 7 || MODE == 8 || MODE == 9) {
+            constexpr int CW = MODE == 6 ? 16 : (MODE == 7 ? 32 : (MODE == 8 ? 8 : 4));
+            ssb::trimv::matvec_tiles<B, CW, NT / 32>(sInv, sR, sPart, threadIdx.x >> 5, threadIdx.x & 31);
             __syncthreads();
             if (tid < B) {
                 double2 s = ssb::trimv::sum_row<B, CW>(sPart, tid);
@@ -119,7 +119,7 @@ __global__ void k_matvec(double2* out, long long* cyc, int reps) {
         __syncthreads();
         if (tid < B) {
             double2 s = sPart[tid];
-            constexpr int Q = MODE == 5 ? 1 : (MODE == 1 ? NT / B : NT / (B / 2));
+            constexpr int Q = MODE == 5 ? 1 : (MODE == 1 ? NT / B : NT / (B / 2));  // unused for tiles
             for (int q = 1; q < Q; q++) { s.x += sPart[q * B + tid].x; s.y += sPart[q * B + tid].y; }
             sR[tid] = make_double2(s.x * 1e-3, s.y * 1e-3);
         }
@@ -169,7 +169,7 @@ __global__ void k_pingpong(volatile unsigned long long* box, long long* res, int
 template <int B, int NT, int MODE>
 void run_mv(const char* name) {
     constexpr int PK = B * (B + 1) / 2;
-    size_t smem = (PK + B + 8 * B) * sizeof(double2);
+    size_t smem = (PK + B + 17 * B) * sizeof(double2);
     double2* out;
     long long* cyc;
     cudaMalloc(&out, 148 * B * sizeof(double2));
@@ -186,7 +186,52 @@ void run_mv(const char* name) {
     cudaFree(cyc);
 }
 
+__global__ void k_lat(double* out, long long* cyc) {
+    double a = threadIdx.x * 1e-3;
+    const double m = 0.999999, c = 1e-9;
+    long long t0 = clock64();
+    for (int i = 0; i < 1024; i++) a = fma(a, m, c);
+    long long t1 = clock64();
+    out[threadIdx.x] = a;
+    if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+
+template <int B, int CW, int A, int S>
+__global__ void k_onetile(double2* out, long long* cyc) {
+    extern __shared__ double2 sm[];
+    constexpr int PK = B * (B + 1) / 2;
+    double2* sInv = sm;
+    double2* sR = sm + PK;
+    double2* sPart = sR + B;
+    for (int i = threadIdx.x; i < PK; i += blockDim.x) sInv[i] = make_double2(1e-3 * (i % 7), 1e-3 * (i % 5));
+    for (int i = threadIdx.x; i < B; i += blockDim.x) sR[i] = make_double2(1.0 + i, 0.5);
+    __syncwarp();
+    long long t0 = clock64();
+    for (int rep = 0; rep < 100; rep++) {
+        ssb::trimv::tile<B, CW>(A, S, sInv, sR, sPart, threadIdx.x);
+        __syncwarp();
+        sR[threadIdx.x % B] = sPart[S * B + 32 * A + threadIdx.x];
+        __syncwarp();
+    }
+    long long t1 = clock64();
+    if (threadIdx.x == 0) cyc[0] = (t1 - t0) / 100;
+    out[threadIdx.x] = sR[threadIdx.x];
+}
+
 int main() {
+    {
+        double* o; long long* c; long long h;
+        cudaMalloc(&o, 4096 * 8); cudaMalloc(&c, 64);
+        k_lat<<<1, 32>>>(o, c); cudaDeviceSynchronize(); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+        printf("DFMA dependent latency: %.2f cycles\n", h / 1024.0);
+        double2* o2; cudaMalloc(&o2, 4096 * 16);
+        cudaFuncSetAttribute(k_onetile<64, 16, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
+        k_onetile<64, 16, 1, 0><<<1, 32, 100000>>>(o2, c); cudaDeviceSynchronize(); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+        printf("one full tile (16 CMAC/lane) single warp: %lld cycles\n", h);
+        cudaFuncSetAttribute(k_onetile<64, 16, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
+        k_onetile<64, 16, 1, 2><<<1, 32, 100000>>>(o2, c); cudaDeviceSynchronize(); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+        printf("one diagonal tile single warp: %lld cycles (%s)\n", h, cudaGetErrorString(cudaGetLastError()));
+    }
     run_mv<128, 512, 0>("matvec");
     run_mv<128, 512, 6>("tiles16");
     run_mv<128, 512, 7>("tiles32");
@@ -194,6 +239,12 @@ int main() {
     run_mv<64, 256, 6>("tiles16");
     run_mv<64, 256, 7>("tiles32");
     run_mv<64, 128, 6>("tiles16");
+    run_mv<64, 256, 8>("tiles8");
+    run_mv<64, 512, 8>("tiles8");
+    run_mv<64, 512, 9>("tiles4");
+    run_mv<64, 512, 6>("tiles16");
+    run_mv<128, 512, 8>("tiles8");
+    run_mv<128, 1024, 8>("tiles8");
     run_mv<128, 512, 2>("matvec-noload");
     run_mv<128, 512, 3>("matvec-loadonly");
     run_mv<128, 512, 4>("barriers+reduce");

@@ -130,3 +130,81 @@ def test_triangular_solves_against_dense():
     ref = np.linalg.solve(U, np.linalg.solve(L, b))
     assert np.abs(T.apply_preconditioner(F, b, small_loops=True) - ref).max() < 1e-11
     assert np.abs(T.apply_preconditioner(F, b) - ref).max() < 1e-11
+
+
+# ---------------------------------------------------------------- iLUTP (reading R13)
+def random_sparse(rng, n, density):
+    """Random complex sparse matrix, far from diagonally dominant (a scaled random
+    permutation is added so that it is nonsingular and pivoting is needed)."""
+    seed = int(rng.integers(1 << 30))
+    A = sp.random(n, n, density=density, random_state=seed, format="csr")
+    A = A + 1j * sp.random(n, n, density=density, random_state=seed + 1, format="csr")
+    perm = rng.permutation(n)
+    A = A + sp.csr_matrix((3.0 + rng.random(n), (np.arange(n), perm)), shape=(n, n))
+    A = sp.csr_matrix(A)
+    A.sort_indices()
+    return A
+
+
+def test_ilutp_permtol0_is_ilut():
+    """permtol = 0 never exchanges columns: bit-identical to ilut (two code paths), and
+    both raise on the same unrecoverable zero pivot."""
+    rng = np.random.default_rng(3)
+    for seed in range(3):
+        for A in (rand_dd(60, 0.15, seed), random_sparse(rng, 60, 0.15)):
+            for d, p in ((0.0, 1e9), (0.05, 3), (1e-3, 10)):
+                try:
+                    F0 = I.ilut(A, d, p)
+                except RuntimeError:
+                    with pytest.raises(RuntimeError):
+                        I.ilutp(A, d, p, 0.0)
+                    continue
+                F1 = I.ilutp(A, d, p, 0.0)
+                assert np.array_equal(F1.perm, np.arange(60))
+                for k in ("Lp", "Lj", "Lx", "Up", "Uj", "Ux"):
+                    assert np.array_equal(getattr(F0, k), getattr(F1, k))
+
+
+def test_ilutp_complete_lu_with_column_pivoting():
+    """d = 0 and unbounded fill: complete LU of A[:, perm] (Saad's ILUTP with no dropping)."""
+    rng = np.random.default_rng(4)
+    for seed in range(3):
+        A = random_sparse(rng, 40, 0.2)
+        F = I.ilutp(A, 0.0, 1e9, 0.5)
+        Lm = (F.L() + sp.identity(40)).toarray()
+        assert np.abs(Lm @ F.U().toarray() - A.toarray()[:, F.perm]).max() <= 1e-10 * np.abs(A.toarray()).max()
+        assert sorted(F.perm.tolist()) == list(range(40))
+        # pivot rule: after the exchange every diagonal is >= permtol * the largest entry of its U row
+        U = F.U().toarray()
+        for i in range(40):
+            assert abs(U[i, i]) >= 0.5 * np.abs(U[i, i:]).max() * (1 - 1e-12)
+
+
+def test_ilutp_factors_zero_diagonal():
+    """[[0, 2], [3, 0]]: ILUT meets an exactly zero pivot (error with d = 0); ILUTP
+    exchanges the columns: A[:, [1, 0]] = I * diag(2, 3)."""
+    A = sp.csr_matrix(np.array([[0, 2], [3, 0]], dtype=complex))
+    with pytest.raises(RuntimeError):
+        I.ilut(A, 0.0, 10)
+    F = I.ilutp(A, 0.0, 10, 0.5)
+    assert F.perm.tolist() == [1, 0]
+    assert np.array_equal(F.U().toarray(), np.array([[2, 0], [0, 3]], dtype=complex))
+    assert F.L().nnz == 0
+
+
+def test_ilutp_hand_worked_exchange():
+    """3x3 by hand, permtol = 0.5, d = 0:
+    A = [[1, 4, 0], [2, 1, 1], [0, 1, 3]]
+    row 0: U part (1, 4, 0); 0.5*4 > 1 -> exchange columns 0 and 1 (perm = [1, 0, 2]);
+           U row 0 = (4 | 1, 0) in positions (0 | 1, 2).
+    row 1 in positions: (a11, a10, a12) = (1, 2, 1); l = 1/4; w = (2 - 1/4, 1 - 0) = (1.75, 1);
+           0.5*1 < 1.75 -> no exchange.  U row 1 = (1.75 | 1).
+    row 2: positions (1, 0, 3); l20 = 1/4; w1 = 0 - 1/4*1 = -0.25, w2 = 3;
+           l21 = -0.25/1.75 = -1/7; w2 = 3 - (-1/7)*1 = 22/7."""
+    A = sp.csr_matrix(np.array([[1, 4, 0], [2, 1, 1], [0, 1, 3]], dtype=complex))
+    F = I.ilutp(A, 0.0, 100, 0.5)
+    assert F.perm.tolist() == [1, 0, 2]
+    U = F.U().toarray()
+    assert np.allclose(U, [[4, 1, 0], [0, 1.75, 1], [0, 0, 22 / 7]], rtol=0, atol=1e-15)
+    Lm = F.L().toarray()
+    assert np.allclose(Lm, [[0, 0, 0], [0.25, 0, 0], [0.25, -1 / 7, 0]], rtol=0, atol=1e-15)

@@ -29,7 +29,8 @@ class Params:
     Gamma_m (1+n_th) D[b], Gamma_m n_th D[b^+]); N_c, N_m are the Fock cut-offs
     (sec. III); w is the trace weight of Eq. (5) (None -> the paper's sec. IV
     rule, the mean of the diagonal of the Liouvillian); drop_tol / fill_factor
-    are the ILUT d, p of sec. II; restart / tol are the GMRES(m) settings.
+    are the ILUT d, p of sec. II and permtol the pivoting threshold of its iLUTP (R13);
+    restart / tol are the GMRES(m) settings.
     """
     N_c: int
     N_m: int
@@ -43,6 +44,7 @@ class Params:
     w: float | None = None
     drop_tol: float = 1e-4
     fill_factor: float = 20.0
+    permtol: float = 0.01         # iLUTP column-exchange threshold (R13)
     restart: int = 30
     tol: float = 1e-10
     max_iter: int = 2000
