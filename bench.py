@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--workload", default="small", choices=["tiny", "small", "medium", "large"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--threads", type=int, default=0, help="host threads for the ILUT setup")
+    ap.add_argument("--dims", default="tiny,small",
+                    help="configs for the time-to-steady-state vs Liouvillian-dim table (rank 0, N = 1)")
     return ap.parse_args()
 
 
@@ -196,6 +198,29 @@ def precond_bytes(si, n):
     return strict * 20 + n * 16 + 2 * ((n + 1) * 8 + 3 * n * 16)
 
 
+def steady_state_vs_dim(names, threads):
+    """Time to steady state (build + setup, then the GMRES solve from x0 = 0) per config;
+    the second half of the BASELINE metric.  Device time of the solve from ss_solve_info,
+    host wall time of build/setup."""
+    import paper_1411_4356_b200 as pb
+
+    rows = []
+    for name in names:
+        p = CONFIGS[name]
+        t0 = time.perf_counter()
+        s = pb.SteadyState(p)
+        s.setup(threads=threads)
+        t1 = time.perf_counter()
+        s.solve()
+        si = s.solve_info
+        rows.append({"config": name, "liouvillian_dim": p.liouvillian_dim, "nnz": s.build_info["nnz"],
+                     "setup_s": t1 - t0, "solve_ms": si["solve_ms"], "iterations": si["iterations"],
+                     "converged": bool(si["converged"]), "rel_residual": si["rel_residual"],
+                     "iterations_per_s": si["iterations"] / (si["solve_ms"] * 1e-3) if si["solve_ms"] else None})
+        s.close()
+    return rows
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -327,6 +352,8 @@ def run_b200(args):
             "gpu_launches": int(launches),
             "clocks": clk,
         }
+        if world == 1 and args.dims:
+            line["time_to_steady_state_vs_dim"] = steady_state_vs_dim(args.dims.split(","), args.threads)
         if not args.no_cpu_baseline and world == 1:
             try:
                 line["cpu_baseline"] = cpu_baseline(args.workload)

@@ -86,6 +86,7 @@ struct Shared {
     int64_t n;
     std::atomic<int64_t> next{0};
     std::atomic<int64_t> front{0};                    // rows < front are published
+    std::atomic<int64_t> swap_version{0};             // bumped by every column exchange
     std::unique_ptr<std::atomic<int64_t>[]> perm;     // position -> original column
     std::unique_ptr<std::atomic<int64_t>[]> iperm;    // original column -> position
     std::vector<RowRef> Lrow, Urow;                   // L: positions; U: original columns
@@ -98,7 +99,8 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
     const int64_t n = S.n;
     std::vector<double2> w(n, make_double2(0.0, 0.0));   // indexed by ORIGINAL column
     std::vector<uint8_t> present(n, 0);
-    std::vector<int64_t> nz, pending, heap;
+    std::vector<int64_t> nz, heap;
+    std::vector<std::pair<int64_t, int64_t>> pending;   // min-heap of (position when keyed, column)
     std::vector<Ent> lbuf, buf;
     nz.reserve(4096);
     pending.reserve(4096);
@@ -106,6 +108,9 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
     buf.reserve(4096);
     lbuf.reserve(4096);
     auto cmp_heap = [](int64_t a, int64_t b) { return a > b; };   // min-heap of positions
+    auto cmp_pend = [](const std::pair<int64_t, int64_t>& a, const std::pair<int64_t, int64_t>& b) {
+        return a.first > b.first;
+    };
     auto by_mag = [](const Ent& a, const Ent& b) { return a.m > b.m || (a.m == b.m && a.j < b.j); };
     auto by_pos = [](const Ent& a, const Ent& b) { return a.j < b.j; };
     const double pt2 = S.permtol * S.permtol;
@@ -127,26 +132,31 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
             w[c] = S.A.val[q];
             present[c] = 1;
             nz.push_back(c);
-            pending.push_back(c);
+            pending.emplace_back(S.iperm[c].load(std::memory_order_relaxed), c);
         }
+        std::make_heap(pending.begin(), pending.end(), cmp_pend);
+        int64_t my_version = -1;   // forces a re-key on the first pass
         const double tau2 = S.drop_tol * S.drop_tol * rowmax2;
 
-        // eliminate final positions < min(F, i) in increasing order as F advances
+        // eliminate final positions < min(F, i) in increasing order as F advances.  Pending
+        // columns are keyed by their position; positions only change through column
+        // exchanges, which bump swap_version before the frontier moves on, so the keys are
+        // refreshed only when that happens (rare).
         for (;;) {
             const int64_t f = S.front.load(std::memory_order_acquire);
-            const int64_t lim = std::min(f, i);
-            size_t keep = 0;
-            for (size_t t = 0; t < pending.size(); t++) {
-                const int64_t c = pending[t];
-                const int64_t p = S.iperm[c].load(std::memory_order_relaxed);
-                if (p < lim) {
-                    heap.push_back(p);
-                    std::push_heap(heap.begin(), heap.end(), cmp_heap);
-                } else {
-                    pending[keep++] = c;
-                }
+            const int64_t ver = S.swap_version.load(std::memory_order_acquire);
+            if (ver != my_version) {
+                for (auto& e : pending) e.first = S.iperm[e.second].load(std::memory_order_relaxed);
+                std::make_heap(pending.begin(), pending.end(), cmp_pend);
+                my_version = ver;
             }
-            pending.resize(keep);
+            const int64_t lim = std::min(f, i);
+            while (!pending.empty() && pending.front().first < lim) {
+                heap.push_back(pending.front().first);
+                std::push_heap(heap.begin(), heap.end(), cmp_heap);
+                std::pop_heap(pending.begin(), pending.end(), cmp_pend);
+                pending.pop_back();
+            }
             if (heap.empty()) {
                 if (f >= i) break;
                 if (S.error_row.load(std::memory_order_relaxed) >= 0) break;
@@ -182,7 +192,8 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
                             heap.push_back(p);
                             std::push_heap(heap.begin(), heap.end(), cmp_heap);
                         } else {
-                            pending.push_back(c);
+                            pending.emplace_back(p, c);
+                            std::push_heap(pending.begin(), pending.end(), cmp_pend);
                         }
                     }
                     const double px = wk.x * u.x - wk.y * u.y;
@@ -233,7 +244,8 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
         const int64_t cdiag = S.perm[i].load(std::memory_order_relaxed);
         double2 di = present[cdiag] ? w[cdiag] : make_double2(0.0, 0.0);
         buf.clear();
-        for (int64_t c : pending) {
+        for (const auto& e : pending) {
+            const int64_t c = e.second;
             if (c == cdiag) continue;
             const double m = mag2(w[c]);
             if (m != 0.0 && !(m < tau2)) buf.push_back(Ent{S.iperm[c].load(std::memory_order_relaxed), c, w[c], m});
@@ -260,6 +272,7 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
             S.perm[tpos].store(cdiag, std::memory_order_relaxed);
             S.iperm[ct].store(i, std::memory_order_relaxed);
             S.iperm[cdiag].store(tpos, std::memory_order_relaxed);
+            S.swap_version.fetch_add(1, std::memory_order_release);
             if (old.x != 0.0 || old.y != 0.0) {
                 buf[tb] = Ent{tpos, cdiag, old, mag2(old)};
             } else {

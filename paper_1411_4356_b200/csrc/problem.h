@@ -46,37 +46,55 @@ struct HostCSR {
 
 // Triangular factor on the device in the block layout of trsv.cu (kernel index space:
 // L as is, U reversed i' = n-1-i so that both are lower triangular; blocks of B rows).
-// near entries per block staged in shared memory by trsv.cu (two stages must fit next to
-// the inverse blocks in 227 KB)
-constexpr int near_cap(int B) { return B <= 32 ? 4096 : 2560; }
+// near entries per block staged in shared memory by trsv.cu: list A (chain SM) and list B
+// (lieutenant SM); two stages of each must fit next to the inverse blocks in 227 KB
+constexpr int near_cap_a(int B) { return B <= 32 ? 2048 : 1536; }
+constexpr int near_cap_b(int B) { return B <= 32 ? 4096 : 3072; }
+
+// one near list on the device (see setup.cpp::build_block_tri)
+struct NearDev {
+    int64_t* bp = nullptr;    // [nblk+1] start of block k's list (multiple of 4 entries)
+    int32_t* col = nullptr;   // kernel-space columns, rows in order
+    double2* val = nullptr;
+    int32_t* loc = nullptr;   // [nblk][B+4] row pointers relative to bp[k]
+    void release() {
+        cudaFree(bp);
+        cudaFree(col);
+        cudaFree(val);
+        cudaFree(loc);
+        *this = NearDev();
+    }
+};
 
 struct TriArgs {
     int64_t n, nblk;
     int32_t rev, B;
-    const int64_t* farptr;    // [n+1] entries of row i' with source block <= k-Q (k = i'/B)
+    const int64_t* farptr;    // [n+1] entries of row i' with source block <= k-Q_k (k = i'/B)
     const int32_t* fcol;      //       kernel-space columns, ascending within a row
     const double2* fval;
-    const int64_t* nbp;       // [nblk+1] start of block k's near list (multiple of 4 entries)
-    const int32_t* ncol;      //       near entries (source blocks k-Q+1 .. k-1), rows in order
-    const double2* nval;
-    const int32_t* nloc;      // [nblk][B+4] row pointers of the near list, relative to nbp[k]
+    const int64_t* nbpA;      // near list A: source blocks k-Dc+1 .. k-1 (chain SM)
+    const int32_t* ncolA;
+    const double2* nvalA;
+    const int32_t* nlocA;
+    const int64_t* nbpB;      // near list B: source blocks k-Q_k+1 .. k-Dc (lieutenant SM)
+    const int32_t* ncolB;
+    const double2* nvalB;
+    const int32_t* nlocB;
     const double2* dinv;      // [nblk][B(B+1)/2] inverse diagonal blocks, packed lower, column-major
     double2* rfar;            // [nblk*B] b - (far part), written by the helper CTAs
     const int64_t* operm;     // [n] output permutation out[operm[i]] = x[i] (ILUTP columns), or null
     uint32_t* fflag;          // [nblk] "rfar of block k is ready" (value = launch epoch)
     unsigned long long* xfront;   // (epoch << 32) | number of blocks of x published
+    int32_t Dc;
 };
 
 struct DevBlockTri {
     int64_t n = 0, nblk = 0, nnz_far = 0, nnz_near = 0, nnz_strict = 0;
-    int B = 0, rev = 0, nt = 0, Q = 0;   // rows per block, reversed (U), threads per CTA, near window
+    int B = 0, rev = 0, nt = 0, Q = 0, Dc = 2;   // rows per block, reversed (U), threads, windows
     int64_t* farptr = nullptr;
     int32_t* fcol = nullptr;
     double2* fval = nullptr;
-    int64_t* nbp = nullptr;
-    int32_t* ncol = nullptr;
-    double2* nval = nullptr;
-    int32_t* nloc = nullptr;
+    NearDev nearA, nearB;
     double2* dinv = nullptr;
     double2* rfar = nullptr;
     uint32_t* fflag = nullptr;
@@ -87,16 +105,16 @@ struct DevBlockTri {
     int grid = 0;
     int64_t nlev = 0;   // row-level dependency levels (diagnostic)
     TriArgs args() const {
-        return TriArgs{n, nblk, rev, B, farptr, fcol, fval, nbp, ncol, nval, nloc, dinv, rfar, operm, fflag, xfront};
+        return TriArgs{n,           nblk,        rev,         B,          farptr,       fcol,        fval,
+                       nearA.bp,    nearA.col,   nearA.val,   nearA.loc,  nearB.bp,     nearB.col,   nearB.val,
+                       nearB.loc,   dinv,        rfar,        operm,      fflag,        xfront,      Dc};
     }
     void release() {
         cudaFree(farptr);
         cudaFree(fcol);
         cudaFree(fval);
-        cudaFree(nbp);
-        cudaFree(ncol);
-        cudaFree(nval);
-        cudaFree(nloc);
+        nearA.release();
+        nearB.release();
         cudaFree(dinv);
         cudaFree(rfar);
         cudaFree(fflag);

@@ -121,7 +121,7 @@ int64_t count_levels(const HostCSR& F, bool upper) {
 // pointers relative to the block start); the in-block entries and the diagonal (1 for
 // L, u_ii for U) form the dense block D_k, whose inverse is stored packed (lower,
 // column-major; column j = rows j..B-1).  The last block is padded with identity rows.
-void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads, DevBlockTri& T,
+void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int dc_in, int threads, DevBlockTri& T,
                      cudaStream_t s) {
     T.release();
     const int64_t n = F.n;
@@ -163,102 +163,134 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
             nin[ip] = c;
         }
     });
-    // per block: the largest window Q_k <= Qmax whose near list fits the stage (Q_k = 1:
-    // no near entries -- every source is then streamed by the helpers, still exact)
+    // per block: the largest window Q_k <= Qmax whose near lists fit their stages.  The near
+    // entries (d < Q_k) split into list A (d < Dc: applied on the chain SM) and list B
+    // (Dc <= d < Q_k: applied by the lieutenant SM of the chain's cluster).  Q_k = 1: no
+    // near entries -- every source is streamed by the helpers (slower, still exact).
     const int qmax = std::max(1, std::min(kMaxQ, q_max));
+    const int dc = std::max(2, std::min(4, dc_in));   // trsv.cu: lieutenant lead 1..3 blocks
     std::vector<int> qk(nblk, qmax);
-    int qmin = qmax;
     parallel_for(nblk, threads, [&](int64_t lo, int64_t hi) {
         for (int64_t k = lo; k < hi; k++) {
             int q = qmax;
             for (; q > 1; q--) {
-                int64_t c = 0;
+                int64_t ca = 0, cb = 0;
                 for (int64_t ip = k * B; ip < std::min(n, (k + 1) * B); ip++)
-                    for (int d = 1; d < q; d++) c += dcnt[(size_t)ip * kMaxQ + d];
-                if (c <= near_cap(B)) break;
+                    for (int d = 1; d < q; d++) (d < dc ? ca : cb) += dcnt[(size_t)ip * kMaxQ + d];
+                if (ca <= near_cap_a(B) && cb <= near_cap_b(B)) break;
             }
             qk[k] = q;
         }
     }, 16);
+    int qmin = qmax;
     for (int64_t k = 0; k < nblk; k++) qmin = std::min(qmin, qk[k]);
     T.Q = qmin;
-    std::vector<int64_t> cnt(n), ncnt(n);   // far / near entries per row
+    T.Dc = dc;
+    std::vector<int64_t> cnt(n), acnt(n), bcnt(n);   // far / list A / list B entries per row
     for (int64_t ip = 0; ip < n; ip++) {
-        int64_t nc = 0;
-        for (int d = 1; d < qk[ip / B]; d++) nc += dcnt[(size_t)ip * kMaxQ + d];
-        ncnt[ip] = nc;
-        cnt[ip] = nin[ip] - nc;
+        int64_t na = 0, nbb = 0;
+        for (int d = 1; d < qk[ip / B]; d++) (d < dc ? na : nbb) += dcnt[(size_t)ip * kMaxQ + d];
+        acnt[ip] = na;
+        bcnt[ip] = nbb;
+        cnt[ip] = nin[ip] - na - nbb;
     }
     std::vector<int64_t>().swap(dcnt);
-    std::vector<int64_t> farptr(n + 1, 0), nbp(nblk + 1, 0), nrow(n + 1, 0);   // nrow: global near row starts
-    std::vector<int32_t> nloc((size_t)nblk * (B + 4), 0);
+    std::vector<int64_t> farptr(n + 1, 0);
     for (int64_t i = 0; i < n; i++) farptr[i + 1] = farptr[i] + cnt[i];
-    for (int64_t k = 0; k < nblk; k++) {
-        int64_t off = 0;
-        for (int r = 0; r < B; r++) {
-            const int64_t ip = k * B + r;
-            nloc[(size_t)k * (B + 4) + r] = (int32_t)off;
-            if (ip < n) {
-                nrow[ip] = nbp[k] + off;
-                off += ncnt[ip];
+    // a near list: per block a padded start, per row a local pointer
+    struct NearHost {
+        std::vector<int64_t> bp, row;   // block starts [nblk+1], global row starts [n]
+        std::vector<int32_t> loc;       // [nblk][B+4]
+    };
+    auto layout = [&](const std::vector<int64_t>& c, NearHost& H) {
+        H.bp.assign(nblk + 1, 0);
+        H.row.assign(n, 0);
+        H.loc.assign((size_t)nblk * (B + 4), 0);
+        for (int64_t k = 0; k < nblk; k++) {
+            int64_t off = 0;
+            for (int r = 0; r < B; r++) {
+                const int64_t ip = k * B + r;
+                H.loc[(size_t)k * (B + 4) + r] = (int32_t)off;
+                if (ip < n) {
+                    H.row[ip] = H.bp[k] + off;
+                    off += c[ip];
+                }
             }
+            for (int r = B; r < B + 4; r++) H.loc[(size_t)k * (B + 4) + r] = (int32_t)off;
+            H.bp[k + 1] = H.bp[k] + ((off + 3) & ~(int64_t)3);
         }
-        for (int r = B; r < B + 4; r++) nloc[(size_t)k * (B + 4) + r] = (int32_t)off;
-        nbp[k + 1] = nbp[k] + ((off + 3) & ~(int64_t)3);
-    }
-    const int64_t nf = farptr[n], nn = nbp[nblk];
+    };
+    NearHost HA, HB;
+    layout(acnt, HA);
+    layout(bcnt, HB);
+    const int64_t nf = farptr[n], nA = HA.bp[nblk], nB = HB.bp[nblk];
     T.nnz_far = nf;
     T.nnz_near = 0;
-    for (int64_t i = 0; i < n; i++) T.nnz_near += ncnt[i];
+    for (int64_t i = 0; i < n; i++) T.nnz_near += acnt[i] + bcnt[i];
     T.nnz_strict = F.nnz() - (upper ? n : 0);
 
+    auto upload_near = [&](const NearHost& H, int64_t total, NearDev& D) {
+        SSB_CUDA(cudaMalloc(&D.bp, (nblk + 1) * sizeof(int64_t)));
+        SSB_CUDA(cudaMalloc(&D.col, std::max<int64_t>(4, total) * sizeof(int32_t)));
+        SSB_CUDA(cudaMalloc(&D.val, std::max<int64_t>(4, total) * sizeof(double2)));
+        SSB_CUDA(cudaMalloc(&D.loc, H.loc.size() * sizeof(int32_t)));
+        SSB_CUDA(cudaMemsetAsync(D.col, 0, std::max<int64_t>(4, total) * sizeof(int32_t), s));   // padding
+        SSB_CUDA(cudaMemcpyAsync(D.bp, H.bp.data(), (nblk + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        SSB_CUDA(cudaMemcpyAsync(D.loc, H.loc.data(), H.loc.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    };
     SSB_CUDA(cudaMalloc(&T.farptr, (n + 1) * sizeof(int64_t)));
     SSB_CUDA(cudaMalloc(&T.fcol, std::max<int64_t>(1, nf) * sizeof(int32_t)));
     SSB_CUDA(cudaMalloc(&T.fval, std::max<int64_t>(1, nf) * sizeof(double2)));
-    SSB_CUDA(cudaMalloc(&T.nbp, (nblk + 1) * sizeof(int64_t)));
-    SSB_CUDA(cudaMalloc(&T.ncol, std::max<int64_t>(4, nn) * sizeof(int32_t)));
-    SSB_CUDA(cudaMalloc(&T.nval, std::max<int64_t>(4, nn) * sizeof(double2)));
-    SSB_CUDA(cudaMalloc(&T.nloc, nloc.size() * sizeof(int32_t)));
+    upload_near(HA, nA, T.nearA);
+    upload_near(HB, nB, T.nearB);
     SSB_CUDA(cudaMalloc(&T.dinv, std::max<int64_t>(1, nblk * PK) * sizeof(double2)));
     SSB_CUDA(cudaMalloc(&T.rfar, std::max<int64_t>(1, nblk * B) * sizeof(double2)));
     SSB_CUDA(cudaMalloc(&T.fflag, std::max<int64_t>(1, nblk) * sizeof(uint32_t)));
     SSB_CUDA(cudaMalloc(&T.xfront, sizeof(unsigned long long)));
     SSB_CUDA(cudaMemsetAsync(T.fflag, 0, std::max<int64_t>(1, nblk) * sizeof(uint32_t), s));
     SSB_CUDA(cudaMemsetAsync(T.xfront, 0, sizeof(unsigned long long), s));
-    SSB_CUDA(cudaMemsetAsync(T.ncol, 0, std::max<int64_t>(4, nn) * sizeof(int32_t), s));   // padding entries
     SSB_CUDA(cudaMemcpyAsync(T.farptr, farptr.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-    SSB_CUDA(cudaMemcpyAsync(T.nbp, nbp.data(), (nblk + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-    SSB_CUDA(cudaMemcpyAsync(T.nloc, nloc.data(), nloc.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     SSB_CUDA(cudaStreamSynchronize(s));
 
-    // entries, in row chunks of ~2^26 (bounded host staging); near rows of a block are
-    // contiguous from nbp[k], so a row chunk maps to one contiguous near range too
+    // entries, in row chunks of ~2^26 (bounded host staging); the rows of a chunk map to
+    // contiguous ranges of the far CSR and of both near lists
     const int64_t kChunk = (int64_t)1 << 26;
-    std::vector<int32_t> fc, nc;
-    std::vector<double2> fv, nv;
+    std::vector<int32_t> fc, ac, bc;
+    std::vector<double2> fv, av, bv;
     for (int64_t r0 = 0; r0 < n;) {
         int64_t r1 = r0 + 1;
-        while (r1 < n && (farptr[r1 + 1] - farptr[r0]) + (nrow[r1] + ncnt[r1] - nrow[r0]) <= kChunk) r1++;
+        while (r1 < n && (farptr[r1 + 1] - farptr[r0]) + (HA.row[r1] + acnt[r1] - HA.row[r0]) +
+                                 (HB.row[r1] + bcnt[r1] - HB.row[r0]) <= kChunk)
+            r1++;
         const int64_t fb = farptr[r0], flen = farptr[r1] - fb;
-        const int64_t nb = nrow[r0], nlen = nrow[r1 - 1] + ncnt[r1 - 1] - nb;
+        const int64_t ab = HA.row[r0], alen = HA.row[r1 - 1] + acnt[r1 - 1] - ab;
+        const int64_t bb = HB.row[r0], blen = HB.row[r1 - 1] + bcnt[r1 - 1] - bb;
         fc.resize(flen);
         fv.resize(flen);
-        nc.assign(nlen, 0);
-        nv.assign(nlen, make_double2(0.0, 0.0));
+        ac.assign(alen, 0);
+        av.assign(alen, make_double2(0.0, 0.0));
+        bc.assign(blen, 0);
+        bv.assign(blen, make_double2(0.0, 0.0));
         parallel_for(r1 - r0, threads, [&](int64_t lo, int64_t hi) {
             for (int64_t ip = r0 + lo; ip < r0 + hi; ip++) {
                 int64_t q0, q1;
                 row_range(ip, q0, q1);
-                const int64_t of = farptr[ip] - fb, on = nrow[ip] - nb;
-                for (int64_t t = 0; t < cnt[ip]; t++) {
+                // row layout (ascending column = descending distance): far | list B | list A | block
+                int64_t t = 0;
+                for (int64_t u = 0; u < cnt[ip]; u++, t++) {
                     const int64_t q = entry(q0, q1, t);
-                    fc[of + t] = (int32_t)kcol(q);
-                    fv[of + t] = F.val[q];
+                    fc[farptr[ip] - fb + u] = (int32_t)kcol(q);
+                    fv[farptr[ip] - fb + u] = F.val[q];
                 }
-                for (int64_t t = 0; t < ncnt[ip]; t++) {
-                    const int64_t q = entry(q0, q1, cnt[ip] + t);
-                    nc[on + t] = (int32_t)kcol(q);
-                    nv[on + t] = F.val[q];
+                for (int64_t u = 0; u < bcnt[ip]; u++, t++) {
+                    const int64_t q = entry(q0, q1, t);
+                    bc[HB.row[ip] - bb + u] = (int32_t)kcol(q);
+                    bv[HB.row[ip] - bb + u] = F.val[q];
+                }
+                for (int64_t u = 0; u < acnt[ip]; u++, t++) {
+                    const int64_t q = entry(q0, q1, t);
+                    ac[HA.row[ip] - ab + u] = (int32_t)kcol(q);
+                    av[HA.row[ip] - ab + u] = F.val[q];
                 }
             }
         });
@@ -266,9 +298,13 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
             SSB_CUDA(cudaMemcpy(T.fcol + fb, fc.data(), flen * sizeof(int32_t), cudaMemcpyHostToDevice));
             SSB_CUDA(cudaMemcpy(T.fval + fb, fv.data(), flen * sizeof(double2), cudaMemcpyHostToDevice));
         }
-        if (nlen > 0) {
-            SSB_CUDA(cudaMemcpy(T.ncol + nb, nc.data(), nlen * sizeof(int32_t), cudaMemcpyHostToDevice));
-            SSB_CUDA(cudaMemcpy(T.nval + nb, nv.data(), nlen * sizeof(double2), cudaMemcpyHostToDevice));
+        if (alen > 0) {
+            SSB_CUDA(cudaMemcpy(T.nearA.col + ab, ac.data(), alen * sizeof(int32_t), cudaMemcpyHostToDevice));
+            SSB_CUDA(cudaMemcpy(T.nearA.val + ab, av.data(), alen * sizeof(double2), cudaMemcpyHostToDevice));
+        }
+        if (blen > 0) {
+            SSB_CUDA(cudaMemcpy(T.nearB.col + bb, bc.data(), blen * sizeof(int32_t), cudaMemcpyHostToDevice));
+            SSB_CUDA(cudaMemcpy(T.nearB.val + bb, bv.data(), blen * sizeof(double2), cudaMemcpyHostToDevice));
         }
         r0 = r1;
     }
@@ -292,7 +328,7 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
                     }
                     int64_t q0, q1;
                     row_range(ip, q0, q1);
-                    for (int64_t t = cnt[ip] + ncnt[ip]; t < q1 - q0; t++) {
+                    for (int64_t t = nin[ip]; t < q1 - q0; t++) {
                         const int64_t q = entry(q0, q1, t);
                         D[(size_t)r * B + (kcol(q) - kb)] = F.val[q];
                     }
@@ -355,14 +391,15 @@ void setup_problem(Problem& P, double drop_tol, double fill_factor, double permt
     if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
     const int B = env_int("SSB_TRSV_B", 32);
     const int QMAX = env_int("SSB_TRSV_Q", 8);
+    const int DC = env_int("SSB_TRSV_DC", 2);
     int64_t levL = 0, levU = 0;
     std::thread lev([&] {
         levL = count_levels(P.hL, false);
         levU = count_levels(P.hU, true);
     });
     try {
-        build_block_tri(P.hL, false, B, QMAX, threads, P.L, s);
-        build_block_tri(P.hU, true, B, QMAX, threads, P.U, s);
+        build_block_tri(P.hL, false, B, QMAX, DC, threads, P.L, s);
+        build_block_tri(P.hU, true, B, QMAX, DC, threads, P.U, s);
         bool identity = true;
         for (int64_t q = 0; q < P.n && identity; q++) identity = P.colperm[q] == q;
         if (!identity) {   // ILUTP exchanged columns: the U substitution scatters x = Pi y

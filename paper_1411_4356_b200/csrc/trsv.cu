@@ -11,7 +11,8 @@
 // sec. 5).  Any row-level substitution pays one synchronisation per level; v1 (one CTA,
 // one barrier per level) ran at 2.6 us per level.
 //
-// v4 (this file): block substitution with one chain SM and the other SMs as helpers.
+// v5 (this file): block substitution on a chain SM, a lieutenant SM of the same thread-
+// block cluster, and the other SMs as helpers.
 // Rows are cut into blocks of B consecutive rows; in the kernel's index space (U
 // reversed at setup, i' = n-1-i, so both factors are lower triangular)
 //     x_k = D_k^{-1} ( b_k - sum_{j<k} T_kj x_j ),
@@ -20,7 +21,10 @@
 //   * "far"  (source blocks <= k-Q): the bulk of the factor bytes.  Helper CTAs stream
 //     them in fixed 32-entry chunks as soon as the chain's completion frontier covers
 //     the chunk's sources, and publish r_k = b_k - (far part) with a release flag;
-//   * "near" (source blocks k-Q+1 .. k-1): a short list per block.
+//   * "near" (source blocks k-Q+1 .. k-1): per block two short lists -- list A (sources
+//     k-Dc+1 .. k-1) applied on the chain SM, list B (k-Q+1 .. k-Dc) applied by the
+//     lieutenant, which receives every x block through DSMEM (st.shared::cluster) and
+//     returns its partial sums of block k the same way, Dc-1 steps ahead of the chain.
 // The chain CTA walks the blocks in order.  Its producer warp waits for r_k's flag and
 // stages D_k^{-1}, the near list and r_k in shared memory with TMA bulk copies
 // (cp.async.bulk + mbarrier, two stages), its 8 compute warps subtract the near part
@@ -107,6 +111,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 constexpr int kTrace = 8;   // stamps per block when tracing (include/ss_b200.h)
+constexpr int kProducerSleep = 32, kPublisherSleep = 32;   // back-off of the polling warps (ns)
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -114,37 +119,67 @@ __device__ __forceinline__ unsigned long long gtime() {
 }
 
 // ------------------------------------------------------------------ configuration
+// ------------------------------------------------------------------ cluster (DSMEM) helpers
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {   // peer CTA's address
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+// 16-byte store into a peer CTA's shared memory that completes 16 bytes of the peer's
+// mbarrier transaction: no fence on the producer side, the consumer waits on the mbarrier
+__device__ __forceinline__ void st_async2(uint32_t addr, double2 v, uint32_t mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(addr),
+                 "d"(v.x), "d"(v.y), "r"(mbar)
+                 : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release;\nbarrier.cluster.wait.acquire;" ::: "memory");
+}
+
+// ------------------------------------------------------------------ configuration
 template <int B>
 struct Cfg {
-    static constexpr int kCompute = 256;              // compute threads of the chain CTA
+    static constexpr int kCompute = 256;              // compute threads per role
     static constexpr int kNT = kCompute + 64;         // + producer warp + publisher warp
     static constexpr int kFarWarps = kCompute / 32;   // helper warps streaming the far part
     static constexpr int kRPW = B / kFarWarps;        // far rows per helper warp
     static constexpr int kGrp = kRPW < 4 ? kRPW : 4;  // far rows gathered together
     static constexpr int kStages = 2;
     static constexpr int kRing = 8;                   // x of the last 8 blocks (Q <= 8)
+    static constexpr int kPbuf = 4;                   // lieutenant partial-sum slots (Dc <= 4)
     static constexpr int kPK = B * (B + 1) / 2;
-    static constexpr int kNCap = near_cap(B);
-    static constexpr int kCW = 16;
+    static constexpr int kCapA = near_cap_a(B), kCapB = near_cap_b(B);
+    static constexpr int kCW = B <= 32 ? 8 : 16;    // mat-vec tile width (4 tiles for B = 32)
     static constexpr int kSegs = B / kCW;
     static constexpr int kNloc = B + 4;               // padded per-block row pointers (int32)
     static constexpr int kTPR = kCompute / B;         // near-phase threads per row
-    // one stage: D_k^{-1} | near columns | near values | near row pointers | r_k
+    // chain stage: D_k^{-1} | list A columns | list A values | list A row pointers | r_k
     static constexpr size_t kOffInv = 0;
-    static constexpr size_t kOffNcol = kOffInv + (size_t)kPK * 16;
-    static constexpr size_t kOffNval = kOffNcol + (size_t)kNCap * 4;
-    static constexpr size_t kOffNloc = kOffNval + (size_t)kNCap * 16;
-    static constexpr size_t kOffRfar = kOffNloc + (size_t)kNloc * 4;
-    static constexpr size_t kStage = kOffRfar + (size_t)B * 16;
+    static constexpr size_t kOffAcol = kOffInv + (size_t)kPK * 16;
+    static constexpr size_t kOffAval = kOffAcol + (size_t)kCapA * 4;
+    static constexpr size_t kOffAloc = kOffAval + (size_t)kCapA * 16;
+    static constexpr size_t kOffRfar = kOffAloc + (size_t)kNloc * 4;
+    static constexpr size_t kChainStage = kOffRfar + (size_t)B * 16;
+    // lieutenant stage: list B columns | list B values | list B row pointers
+    static constexpr size_t kOffBcol = 0;
+    static constexpr size_t kOffBval = kOffBcol + (size_t)kCapB * 4;
+    static constexpr size_t kOffBloc = kOffBval + (size_t)kCapB * 16;
+    static constexpr size_t kLtStage = kOffBloc + (size_t)kNloc * 4;
+    static constexpr size_t kStage = kChainStage > kLtStage ? kChainStage : kLtStage;
     static constexpr size_t kOffRing = kStage * kStages;
     static constexpr size_t kOffR = kOffRing + (size_t)kRing * B * 16;
     static constexpr size_t kOffPart = kOffR + (size_t)B * 16;
-    static constexpr size_t kOffRowP = kOffPart + (size_t)kSegs * B * 16;
+    static constexpr size_t kOffPbuf = kOffPart + (size_t)kSegs * B * 16;
+    static constexpr size_t kOffRowP = kOffPbuf + (size_t)kPbuf * B * 16;
     static constexpr size_t kOffRowL = kOffRowP + (size_t)B * 8;
     static constexpr size_t kOffBar = kOffRowL + (size_t)B * 4;
-    static constexpr size_t kSmem = kOffBar + 16 * kStages + 64;
+    static constexpr size_t kOffXbar = kOffBar + 16 * kStages + 64;   // lieutenant: x block j landed
+    static constexpr size_t kOffPbar = kOffXbar + 8 * kRing;          // chain: partial of block k landed
+    static constexpr size_t kSmem = kOffPbar + 8 * kPbuf;
     static_assert(kCompute % B == 0 && B % kFarWarps == 0 && kRPW % kGrp == 0 && B % 32 == 0, "layout");
-    static_assert(kStage % 16 == 0 && kOffNval % 16 == 0 && kOffNloc % 16 == 0 && kOffRfar % 16 == 0, "TMA");
+    static_assert(kChainStage % 16 == 0 && kLtStage % 16 == 0 && kOffAval % 16 == 0 && kOffAloc % 16 == 0 &&
+                      kOffRfar % 16 == 0 && kOffBval % 16 == 0 && kOffBloc % 16 == 0,
+                  "TMA alignment");
 };
 
 // Helper-side wait: return once the chain frontier (blocks < F published) reaches target.
@@ -174,6 +209,56 @@ __device__ __forceinline__ void helper_wait(int target, int* sF, int* sLock, con
     __syncwarp();   // every lane's later loads follow the acquire chain
 }
 
+// Near products of one block's list (row pointers loc, kTPR threads per row, contiguous
+// parts): returns the row sum on lane q == 0 of each row group, x read from the ring.
+template <int B>
+__device__ __forceinline__ double2 near_rows(const int32_t* loc, const int32_t* col, const double2* val,
+                                             const double2* ring, int tid) {
+    using C = Cfg<B>;
+    constexpr int kRingMask = C::kRing * B - 1;
+    const int r = tid / C::kTPR, q = tid % C::kTPR;
+    const int lo = loc[r], hi = loc[r + 1], len = hi - lo;
+    const int e0 = lo + (q * len) / C::kTPR, e1 = lo + ((q + 1) * len) / C::kTPR;
+    double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
+    int e = e0;
+    for (; e + 4 <= e1; e += 4) {
+        const int c0 = col[e], c1 = col[e + 1], c2 = col[e + 2], c3 = col[e + 3];
+        const double2 v0 = val[e], v1 = val[e + 1], v2 = val[e + 2], v3 = val[e + 3];
+        const double2 x0 = ring[c0 & kRingMask], x1 = ring[c1 & kRingMask];
+        const double2 x2 = ring[c2 & kRingMask], x3 = ring[c3 & kRingMask];
+        acc = cfma(acc, v0, x0);
+        acc2 = cfma(acc2, v1, x1);
+        acc = cfma(acc, v2, x2);
+        acc2 = cfma(acc2, v3, x3);
+    }
+    for (; e < e1; e++) acc = cfma(acc, val[e], ring[col[e] & kRingMask]);
+    acc = cadd(acc, acc2);
+#pragma unroll
+    for (int o = 1; o < C::kTPR; o <<= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    return acc;
+}
+
+// Stage one near list block (TMA): columns (padded to 4), values, row pointers.
+__device__ __forceinline__ uint32_t stage_near(unsigned char* col_dst, unsigned char* val_dst,
+                                               unsigned char* loc_dst, const int64_t* bp, const int32_t* col,
+                                               const double2* val, const int32_t* loc, int k, int nloc,
+                                               uint64_t* bar, bool issue) {
+    const int64_t b0 = bp[k];
+    const uint32_t cnt = (uint32_t)(bp[k + 1] - b0);   // already a multiple of 4
+    const uint32_t bytes = cnt * 20 + (uint32_t)nloc * 4;
+    if (issue) {
+        if (cnt) {
+            bulk_g2s(col_dst, col + b0, cnt * 4, bar);
+            bulk_g2s(val_dst, val + b0, cnt * 16, bar);
+        }
+        bulk_g2s(loc_dst, loc + (int64_t)k * nloc, (uint32_t)nloc * 4, bar);
+    }
+    return bytes;
+}
+
 template <int B>
 __global__ void __launch_bounds__(Cfg<B>::kNT, 1)
 k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, double2* x, uint32_t epoch,
@@ -182,13 +267,20 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
     uint64_t* empty = full + C::kStages;
-    int* sDone = reinterpret_cast<int*>(empty + C::kStages);
-    int* sF = sDone + 1;
+    int* sDone = reinterpret_cast<int*>(empty + C::kStages);   // chain: blocks of x done
+    int* sF = sDone + 1;                                          // helpers: frontier view
     int* sLock = sDone + 2;
+    int* sPub = sDone + 3;                                        // chain: blocks published to global
+    uint64_t* xbar = reinterpret_cast<uint64_t*>(smem + C::kOffXbar);
+    uint64_t* pbar = reinterpret_cast<uint64_t*>(smem + C::kOffPbar);
+    double2* ring = reinterpret_cast<double2*>(smem + C::kOffRing);
+    double2* pbuf = reinterpret_cast<double2*>(smem + C::kOffPbuf);
+    constexpr int kRingMask = C::kRing * B - 1;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t n = a.n;
     const int nblk = (int)a.nblk;
+    const int Dc = a.Dc;
     const bool rev = a.rev != 0;
     auto phys = [&](int64_t i) -> int64_t { return rev ? n - 1 - i : i; };
 
@@ -200,131 +292,168 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
         *sDone = 0;
         *sF = 0;
         *sLock = 0;
+        *sPub = 0;
+        for (int j = 0; j < C::kRing; j++) mbar_init(xbar + j, 1);
+        for (int j = 0; j < C::kPbuf; j++) mbar_init(pbar + j, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncthreads();
+    cluster_sync();   // counters of both CTAs of a cluster initialised before any DSMEM access
 
-    if (blockIdx.x == 0) {
-        // ============================================================ chain CTA
-        if (warp == C::kCompute / 32) {   // producer: stage block k's operands (TMA)
+    if (blockIdx.x <= 1) {
+        const bool chain = blockIdx.x == 0;
+        const uint32_t peer = chain ? 1u : 0u;
+        if (warp == C::kCompute / 32) {
+            // ------------------------------------------------ producer: TMA staging
             if (lane == 0) {
                 for (int k = 0; k < nblk; k++) {
                     const int s = k % C::kStages;
                     if (k >= C::kStages) mbar_wait(empty + s, (uint32_t)((k / C::kStages - 1) & 1));
-                    while (ld_acquire(a.fflag + k) != epoch) __nanosleep(20);
-                    if (trace) trace[(int64_t)k * kTrace + 5] = gtime();
-                    fence_proxy_async();   // r_k (generic-proxy stores of a helper) -> TMA reads
-                    const int64_t nb0 = a.nbp[k];
-                    const uint32_t cnt = (uint32_t)(a.nbp[k + 1] - nb0);
-                    const uint32_t cpad = (cnt + 3u) & ~3u;
                     unsigned char* st = smem + C::kStage * s;
-                    const uint32_t bytes = (uint32_t)(C::kPK * 16 + cpad * 4 + cnt * 16 + C::kNloc * 4 + B * 16);
-                    mbar_expect_tx(full + s, bytes);
-                    bulk_g2s(st + C::kOffInv, a.dinv + (int64_t)k * C::kPK, C::kPK * 16, full + s);
-                    if (cnt) {
-                        bulk_g2s(st + C::kOffNcol, a.ncol + nb0, cpad * 4, full + s);
-                        bulk_g2s(st + C::kOffNval, a.nval + nb0, cnt * 16, full + s);
+                    if (chain) {
+                        while (ld_acquire(a.fflag + k) != epoch) __nanosleep(kProducerSleep);
+                        if (trace) trace[(int64_t)k * kTrace + 5] = gtime();
+                        fence_proxy_async();   // r_k (generic-proxy stores of a helper) -> TMA reads
+                        const uint32_t nb = stage_near(nullptr, nullptr, nullptr, a.nbpA, a.ncolA, a.nvalA,
+                                                       a.nlocA, k, C::kNloc, full + s, false);
+                        mbar_expect_tx(full + s, (uint32_t)(C::kPK * 16 + B * 16) + nb);
+                        bulk_g2s(st + C::kOffInv, a.dinv + (int64_t)k * C::kPK, C::kPK * 16, full + s);
+                        stage_near(st + C::kOffAcol, st + C::kOffAval, st + C::kOffAloc, a.nbpA, a.ncolA, a.nvalA,
+                                   a.nlocA, k, C::kNloc, full + s, true);
+                        bulk_g2s(st + C::kOffRfar, a.rfar + (int64_t)k * B, B * 16, full + s);
+                    } else {
+                        const uint32_t nb = stage_near(nullptr, nullptr, nullptr, a.nbpB, a.ncolB, a.nvalB,
+                                                       a.nlocB, k, C::kNloc, full + s, false);
+                        mbar_expect_tx(full + s, nb);
+                        stage_near(st + C::kOffBcol, st + C::kOffBval, st + C::kOffBloc, a.nbpB, a.ncolB, a.nvalB,
+                                   a.nlocB, k, C::kNloc, full + s, true);
                     }
-                    bulk_g2s(st + C::kOffNloc, a.nloc + (int64_t)k * C::kNloc, C::kNloc * 4, full + s);
-                    bulk_g2s(st + C::kOffRfar, a.rfar + (int64_t)k * B, B * 16, full + s);
                 }
             }
-            return;
-        }
-        if (warp == C::kCompute / 32 + 1) {   // publisher: advance the global frontier word
-            if (lane == 0) {
+        } else if (warp == C::kCompute / 32 + 1) {
+            // ------------------------------------------------ publisher (chain only): copies
+            // finished x blocks from the ring to global memory (and through the iLUTP column
+            // permutation to the output), then advances the gpu-scope frontier word
+            if (chain) {
                 int published = 0;
                 while (published < nblk) {
                     const int d = ld_acq_cta(sDone);
                     if (d > published) {
-                        st_release64(a.xfront, ((unsigned long long)epoch << 32) | (unsigned)d);
-
+                        for (int j = published; j < d; j++)
+                            for (int r = lane; r < B; r += 32) {
+                                const int64_t i = (int64_t)j * B + r;
+                                if (i < n) {
+                                    const double2 v = ring[i & kRingMask];
+                                    const int64_t pi = phys(i);
+                                    x[pi] = v;
+                                    if (a.operm) out[a.operm[pi]] = v;
+                                }
+                            }
+                        __syncwarp();
+                        if (lane == 0) {
+                            st_release64(a.xfront, ((unsigned long long)epoch << 32) | (unsigned)d);
+                            st_rel_cta(sPub, d);
+                        }
                         published = d;
                     } else {
-                        __nanosleep(20);
+                        __nanosleep(kPublisherSleep);
                     }
                 }
             }
-            return;
-        }
-        // compute warps
-        double2* ring = reinterpret_cast<double2*>(smem + C::kOffRing);
-        double2* sR = reinterpret_cast<double2*>(smem + C::kOffR);
-        double2* sPart = reinterpret_cast<double2*>(smem + C::kOffPart);
-        constexpr int kRingMask = C::kRing * B - 1;
-        for (int k = 0; k < nblk; k++) {
-            const int s = k % C::kStages;
-            unsigned char* st = smem + C::kStage * s;
-            const double2* sInv = reinterpret_cast<const double2*>(st + C::kOffInv);
-            const int32_t* sNcol = reinterpret_cast<const int32_t*>(st + C::kOffNcol);
-            const double2* sNval = reinterpret_cast<const double2*>(st + C::kOffNval);
-            const int32_t* sNloc = reinterpret_cast<const int32_t*>(st + C::kOffNloc);
-            const double2* sRfar = reinterpret_cast<const double2*>(st + C::kOffRfar);
-            mbar_wait(full + s, (uint32_t)((k / C::kStages) & 1));
-            if (trace && tid == 0) trace[(int64_t)k * kTrace + 0] = gtime();
-            // near part: kTPR threads per row, contiguous parts of the row's list
-            {
-                const int r = tid / C::kTPR, q = tid % C::kTPR;
-                const int lo = sNloc[r], hi = sNloc[r + 1], len = hi - lo;
-                const int e0 = lo + (q * len) / C::kTPR, e1 = lo + ((q + 1) * len) / C::kTPR;
-                // 4 entries per trip: the column, value and x loads of a batch are issued
-                // together (two dependent shared-memory round trips per batch, not per entry)
-                double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
-                int e = e0;
-                for (; e + 4 <= e1; e += 4) {
-                    const int c0 = sNcol[e], c1 = sNcol[e + 1], c2 = sNcol[e + 2], c3 = sNcol[e + 3];
-                    const double2 v0 = sNval[e], v1 = sNval[e + 1], v2 = sNval[e + 2], v3 = sNval[e + 3];
-                    const double2 x0 = ring[c0 & kRingMask], x1 = ring[c1 & kRingMask];
-                    const double2 x2 = ring[c2 & kRingMask], x3 = ring[c3 & kRingMask];
-                    acc = cfma(acc, v0, x0);
-                    acc2 = cfma(acc2, v1, x1);
-                    acc = cfma(acc, v2, x2);
-                    acc2 = cfma(acc2, v3, x3);
-                }
-                for (; e < e1; e++) acc = cfma(acc, sNval[e], ring[sNcol[e] & kRingMask]);
-                acc = cadd(acc, acc2);
+        } else if (chain) {
+            // ------------------------------------------------ chain compute warps
+            double2* sR = reinterpret_cast<double2*>(smem + C::kOffR);
+            double2* sPart = reinterpret_cast<double2*>(smem + C::kOffPart);
+            const uint32_t peer_ring = mapa(smem_u32(ring), peer);
+            const uint32_t peer_xbar = mapa(smem_u32(xbar), peer);
+            for (int k = 0; k < nblk; k++) {
+                const int s = k % C::kStages;
+                unsigned char* st = smem + C::kStage * s;
+                const double2* sInv = reinterpret_cast<const double2*>(st + C::kOffInv);
+                const double2* sRfar = reinterpret_cast<const double2*>(st + C::kOffRfar);
+                mbar_wait(full + s, (uint32_t)((k / C::kStages) & 1));
+                if (trace && tid == 0) trace[(int64_t)k * kTrace + 0] = gtime();
+                const double2 accA = near_rows<B>(reinterpret_cast<const int32_t*>(st + C::kOffAloc),
+                                                  reinterpret_cast<const int32_t*>(st + C::kOffAcol),
+                                                  reinterpret_cast<const double2*>(st + C::kOffAval), ring, tid);
                 if (trace && tid == 0) trace[(int64_t)k * kTrace + 6] = gtime();
-#pragma unroll
-                for (int o = 1; o < C::kTPR; o <<= 1) {
-                    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-                    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+                if (tid % C::kTPR == 0) {
+                    const int r = tid / C::kTPR, pk = k % C::kPbuf;
+                    // the lieutenant's partial of block k (B values, st.async) lands on pbar[pk]
+                    if (r == 0) mbar_expect_tx(pbar + pk, (uint32_t)(B * 16));
+                    mbar_wait(pbar + pk, (uint32_t)((k / C::kPbuf) & 1));
+                    sR[r] = csub(csub(sRfar[r], accA), pbuf[pk * B + r]);
                 }
-                if (q == 0) sR[r] = csub(sRfar[r], acc);
+                bar_compute(C::kCompute);
+                if (trace && tid == 0) trace[(int64_t)k * kTrace + 1] = gtime();
+                trimv::matvec_tiles<B, C::kCW, C::kCompute / 32>(sInv, sR, sPart, warp, lane);
+                bar_compute(C::kCompute);
+                if (trace && tid == 0) trace[(int64_t)k * kTrace + 2] = gtime();
+                if (tid == 0) mbar_arrive(empty + s);   // stage s may be refilled
+                if (tid < B) {
+                    // ring slot of block k held block k-8: the publisher must have copied it
+                    if (k >= C::kRing)
+                        while (ld_acq_cta(sPub) < k - C::kRing + 1) {
+                        }
+                    const double2 v = trimv::sum_row<B, C::kCW>(sPart, tid);
+                    const int64_t i = (int64_t)k * B + tid;
+                    ring[i & kRingMask] = v;
+                    st_async2(peer_ring + (uint32_t)((i & kRingMask) * 16), v,
+                              peer_xbar + (uint32_t)((k % C::kRing) * 8));   // lieutenant's ring
+                }
+                bar_compute(C::kCompute);
+                if (tid == 0) {
+                    st_rel_cta(sDone, k + 1);   // the publisher copies x_k to global memory
+                    if (trace) trace[(int64_t)k * kTrace + 3] = gtime();
+                }
+            }
+        } else {
+            // ------------------------------------------------ lieutenant compute warps
+            const uint32_t peer_pbuf = mapa(smem_u32(pbuf), peer);
+            const uint32_t peer_pbar = mapa(smem_u32(pbar), peer);
+            int xseen = 0;   // x blocks < xseen have landed in the ring
+            for (int k = 0; k < nblk; k++) {
+                const int s = k % C::kStages;
+                unsigned char* st = smem + C::kStage * s;
+                mbar_wait(full + s, (uint32_t)((k / C::kStages) & 1));
+                // list B of block k reads x of blocks <= k - Dc: consume their arrivals in
+                // order (each xbar phase exactly once); pbuf slot k % 4 was last read by
+                // the chain for block k - 4 < k - Dc + 1
+                for (; xseen <= k - Dc; xseen++) {
+                    const int j = xseen % C::kRing;
+                    if (tid == 0) mbar_expect_tx(xbar + j, (uint32_t)(B * 16));
+                    mbar_wait(xbar + j, (uint32_t)((xseen / C::kRing) & 1));
+                }
                 if (trace && tid == 0) trace[(int64_t)k * kTrace + 7] = gtime();
-            }
-            bar_compute(C::kCompute);
-            if (trace && tid == 0) trace[(int64_t)k * kTrace + 1] = gtime();
-            trimv::matvec_tiles<B, C::kCW, C::kCompute / 32>(sInv, sR, sPart, warp, lane);
-            bar_compute(C::kCompute);
-            if (trace && tid == 0) trace[(int64_t)k * kTrace + 2] = gtime();
-            if (tid == 0) mbar_arrive(empty + s);   // stage s may be refilled
-            if (tid < B) {
-                const double2 v = trimv::sum_row<B, C::kCW>(sPart, tid);
-                const int64_t i = (int64_t)k * B + tid;
-                ring[i & kRingMask] = v;
-                if (i < n) {
-                    const int64_t pi = phys(i);
-                    x[pi] = v;                              // kernel-space x (helpers read it)
-                    if (a.operm) out[a.operm[pi]] = v;      // ILUTP: undo the column exchanges
+                const double2 accB = near_rows<B>(reinterpret_cast<const int32_t*>(st + C::kOffBloc),
+                                                  reinterpret_cast<const int32_t*>(st + C::kOffBcol),
+                                                  reinterpret_cast<const double2*>(st + C::kOffBval), ring, tid);
+                if (tid % C::kTPR == 0) {
+                    const int pk = k % C::kPbuf;
+                    st_async2(peer_pbuf + (uint32_t)((pk * B + tid / C::kTPR) * 16), accB, peer_pbar + (uint32_t)(pk * 8));
                 }
+                bar_compute(C::kCompute);
+                if (tid == 0) mbar_arrive(empty + s);
             }
-            bar_compute(C::kCompute);
-            if (tid == 0) {
-                st_rel_cta(sDone, k + 1);
-                if (trace) trace[(int64_t)k * kTrace + 3] = gtime();
+            for (; xseen < nblk; xseen++) {   // drain the remaining arrivals before leaving
+                const int j = xseen % C::kRing;
+                if (tid == 0) mbar_expect_tx(xbar + j, (uint32_t)(B * 16));
+                mbar_wait(xbar + j, (uint32_t)((xseen / C::kRing) & 1));
             }
         }
+        // all threads of both CTAs: no CTA of the cluster leaves while its peer may still
+        // access its shared memory
+        __syncwarp();
+        cluster_sync();
         return;
     }
 
     // ================================================================ helper CTAs
     if (warp >= C::kFarWarps) return;
-    const int H = gridDim.x - 1;
+    const int H = gridDim.x - 2;
     int64_t* sRowP = reinterpret_cast<int64_t*>(smem + C::kOffRowP);
     int32_t* sRowL = reinterpret_cast<int32_t*>(smem + C::kOffRowL);
-    for (int k = blockIdx.x - 1; k < nblk; k += H) {
+    for (int k = blockIdx.x - 2; k < nblk; k += H) {
         const int64_t row0 = (int64_t)k * B;
-
         double2 acc[C::kRPW];
         int64_t* wp = sRowP + warp * C::kRPW;
         int32_t* wl = sRowL + warp * C::kRPW;
@@ -395,13 +524,28 @@ void prepare(DevBlockTri& T) {
     using C = Cfg<B>;
     auto fn = k_chain_trsv<B>;
     SSB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem));
-    int dev = 0, sms = 0, per = 0;
+    SSB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+    int dev = 0, sms = 0;
     SSB_CUDA(cudaGetDevice(&dev));
     SSB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, C::kNT, C::kSmem));
-    SSB_CHECK(per >= 1, SS_ERR_CUDA, "block trsv kernel does not fit on an SM");
-    // chain CTA + helpers; one CTA per SM (more helpers than blocks are useless)
-    T.grid = (int)std::max<int64_t>(2, std::min<int64_t>(T.nblk + 1, (int64_t)sms));
+    // clusters of 2 (chain + lieutenant, then pairs of helpers), one CTA per SM; every
+    // cluster must be resident at once (the CTAs spin on one another)
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(C::kNT);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int clusters = 0;
+    cfg.gridDim = dim3((unsigned)(sms & ~1));
+    SSB_CUDA(cudaOccupancyMaxActiveClusters(&clusters, fn, &cfg));
+    SSB_CHECK(clusters >= 2, SS_ERR_CUDA, "block trsv: fewer than two co-resident CTA pairs");
+    const int64_t want = std::max<int64_t>(4, 2 * ((T.nblk + 3) / 2));   // chain, lieutenant, >= 2 helpers
+    T.grid = (int)std::min<int64_t>(want, 2 * (int64_t)clusters);
     T.nt = C::kNT;
 }
 
@@ -414,8 +558,19 @@ void launch(DevBlockTri& T, const double2* b, double2* x, cudaStream_t s, unsign
     TriArgs a = T.args();
     uint32_t ep = T.epoch;
     double2* xw = T.operm ? T.xwork : x;
-    void* args[] = {(void*)&a, (void*)&b, (void*)&x, (void*)&xw, (void*)&ep, (void*)&trace};
-    SSB_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3(T.grid), dim3(C::kNT), args, C::kSmem, s));
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(T.grid);
+    cfg.blockDim = dim3(C::kNT);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SSB_CUDA(cudaLaunchKernelEx(&cfg, fn, a, b, x, xw, ep, trace));
     SSB_LAUNCHED();
 }
 

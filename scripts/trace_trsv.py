@@ -41,14 +41,12 @@ def main():
             "total_us": float(tr[:, 3].max() / 1e3),
             "step_ns": med(tr[1:, 3] - tr[:-1, 3]),
             "chain_wait_ns": med(rel[:, 0] - done_prev),
-            "near_ns": med(rel[:, 1] - rel[:, 0]),
+            "nearA_ns": med(tr[:, 6] - tr[:, 0]),
+            "pbuf_wait_and_bar_ns": med(tr[:, 1] - tr[:, 6]),
             "matvec_ns": med(rel[:, 2] - rel[:, 1]),
             "store_ns": med(rel[:, 3] - rel[:, 2]),
+            "lieutenant_start_minus_chain_start_ns": med(tr[:, 7] - tr[:, 0]),
             "helper_publish_minus_prev_done_ns": med(rel[:, 4] - done_prev),
-            "producer_sees_flag_after_publish_ns": med(tr[:, 5] - tr[:, 4]),
-            "near_loop_tid0_ns": med(tr[:, 6] - tr[:, 0]),
-            "near_shfl_tid0_ns": med(tr[:, 7] - tr[:, 6]),
-            "near_barrier_ns": med(tr[:, 1] - tr[:, 7]),
             "chain_waited_on_helpers_frac": float(np.mean(rel[:, 5] > done_prev)),
             "first_blocks": tr[:3].tolist(),
         }

@@ -179,3 +179,29 @@ def test_kernel_launch_counter_moves(cuda):
     s = m.SteadyState(CONFIGS["tiny"]).setup().solve()
     assert m.ss_kernel_launches() > before + 10
     s.close()
+
+
+def test_sweep_points_on_gpu(cuda):
+    """The detuning sweep driver (sweep.py, world size 1) on a few jittered tiny points:
+    every point's observables equal the oracle's direct solve within the bound above."""
+    from paper_1411_4356_b200.sweep import run_sweep
+    pts = [tiny_params(3, 8, Delta=d, n_th=0.2) for d in (-1.0, -0.25, 0.5)]
+    table = run_sweep(pts)
+    for row, p in zip(table, pts):
+        assert row[0] == p.Delta and row[5] == 1.0 and row[4] <= p.tol
+        ref = ss.solve_direct(p)
+        ra, rb = ss.expect(ref, p)
+        assert abs(row[1] - ra) <= 1e-7 and abs(row[2] - rb) <= 1e-6
+
+
+def test_trace_abi(cuda):
+    """ss_debug_trace_trsv returns one row of 8 stamps per block of the substitution."""
+    torch = cuda
+    s = pb().SteadyState(CONFIGS["tiny"]).setup()
+    x = torch.randn(s.n, dtype=torch.complex128, device="cuda")
+    y = torch.empty_like(x)
+    tr = pb().ss_debug_trace_trsv(s.handle, 0, x.data_ptr(), y.data_ptr())
+    assert tr.shape == ((s.n + 31) // 32, 8)
+    ref = s.precond(x, 0)
+    assert torch.equal(y, ref)      # tracing does not change the result
+    s.close()
