@@ -48,7 +48,7 @@ struct HostCSR {
 // L as is, U reversed i' = n-1-i so that both are lower triangular; blocks of B rows).
 // near entries per block staged in shared memory by trsv.cu: list A (chain SM) and list B
 // (lieutenant SM); two stages of each must fit next to the inverse blocks in 227 KB
-constexpr int near_cap_a(int B) { return B <= 32 ? 2048 : 1536; }
+constexpr int near_cap_a(int B) { return B <= 32 ? 1024 : 1024; }
 constexpr int near_cap_b(int B) { return B <= 32 ? 4096 : 3072; }
 
 // one near list on the device (see setup.cpp::build_block_tri)
@@ -81,6 +81,7 @@ struct TriArgs {
     const double2* nvalB;
     const int32_t* nlocB;
     const double2* dinv;      // [nblk][B(B+1)/2] inverse diagonal blocks, packed lower, column-major
+    const double2* G;         // [nblk][2][B*B] D_k^{-1} T_{k,k-d}, d = 1, 2, column-major
     double2* rfar;            // [nblk*B] b - (far part), written by the helper CTAs
     const int64_t* operm;     // [n] output permutation out[operm[i]] = x[i] (ILUTP columns), or null
     uint32_t* fflag;          // [nblk] "rfar of block k is ready" (value = launch epoch)
@@ -96,6 +97,7 @@ struct DevBlockTri {
     double2* fval = nullptr;
     NearDev nearA, nearB;
     double2* dinv = nullptr;
+    double2* G = nullptr;
     double2* rfar = nullptr;
     uint32_t* fflag = nullptr;
     unsigned long long* xfront = nullptr;
@@ -107,7 +109,8 @@ struct DevBlockTri {
     TriArgs args() const {
         return TriArgs{n,           nblk,        rev,         B,          farptr,       fcol,        fval,
                        nearA.bp,    nearA.col,   nearA.val,   nearA.loc,  nearB.bp,     nearB.col,   nearB.val,
-                       nearB.loc,   dinv,        rfar,        operm,      fflag,        xfront,      Dc};
+                       nearB.loc,   dinv,        G,           rfar,       operm,        fflag,       xfront,
+                       Dc};
     }
     void release() {
         cudaFree(farptr);
@@ -116,6 +119,7 @@ struct DevBlockTri {
         nearA.release();
         nearB.release();
         cudaFree(dinv);
+        cudaFree(G);
         cudaFree(rfar);
         cudaFree(fflag);
         cudaFree(xfront);

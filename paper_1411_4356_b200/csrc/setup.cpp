@@ -163,21 +163,22 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int dc_in, 
             nin[ip] = c;
         }
     });
-    // per block: the largest window Q_k <= Qmax whose near lists fit their stages.  The near
-    // entries (d < Q_k) split into list A (d < Dc: applied on the chain SM) and list B
-    // (Dc <= d < Q_k: applied by the lieutenant SM of the chain's cluster).  Q_k = 1: no
-    // near entries -- every source is streamed by the helpers (slower, still exact).
-    const int qmax = std::max(1, std::min(kMaxQ, q_max));
-    const int dc = std::max(2, std::min(4, dc_in));   // trsv.cu: lieutenant lead 1..3 blocks
+    // Split of the entries left of block k by source distance d (trsv.cu v6):
+    //   d = 1, 2       -> G1_k = D_k^{-1} T_{k,k-1}, G2_k = D_k^{-1} T_{k,k-2} (dense B x B;
+    //                     the chain warp and the t warp of the chain CTA)
+    //   3 <= d < Q_k   -> list B (the lieutenant CTAs of the chain's cluster)
+    //   d >= Q_k       -> far (the helper CTAs)
+    // Q_k is the largest Q <= Qmax (>= 3) whose list B fits its shared-memory stage.
+    const int qmax = std::max(3, std::min(kMaxQ, q_max));
     std::vector<int> qk(nblk, qmax);
     parallel_for(nblk, threads, [&](int64_t lo, int64_t hi) {
         for (int64_t k = lo; k < hi; k++) {
             int q = qmax;
-            for (; q > 1; q--) {
-                int64_t ca = 0, cb = 0;
+            for (; q > 3; q--) {
+                int64_t cb = 0;
                 for (int64_t ip = k * B; ip < std::min(n, (k + 1) * B); ip++)
-                    for (int d = 1; d < q; d++) (d < dc ? ca : cb) += dcnt[(size_t)ip * kMaxQ + d];
-                if (ca <= near_cap_a(B) && cb <= near_cap_b(B)) break;
+                    for (int d = 3; d < q; d++) cb += dcnt[(size_t)ip * kMaxQ + d];
+                if (cb <= near_cap_b(B)) break;
             }
             qk[k] = q;
         }
@@ -185,14 +186,17 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int dc_in, 
     int qmin = qmax;
     for (int64_t k = 0; k < nblk; k++) qmin = std::min(qmin, qk[k]);
     T.Q = qmin;
-    T.Dc = dc;
-    std::vector<int64_t> cnt(n), acnt(n), bcnt(n);   // far / list A / list B entries per row
+    T.Dc = 3;
+    // per row: far / list A (unused: 0) / list B / G1 / G2 entries
+    std::vector<int64_t> cnt(n), acnt(n, 0), bcnt(n), gcnt(n), g2cnt(n);
     for (int64_t ip = 0; ip < n; ip++) {
-        int64_t na = 0, nbb = 0;
-        for (int d = 1; d < qk[ip / B]; d++) (d < dc ? na : nbb) += dcnt[(size_t)ip * kMaxQ + d];
-        acnt[ip] = na;
+        const int q = qk[ip / B];
+        int64_t nbb = 0;
+        for (int d = 3; d < q; d++) nbb += dcnt[(size_t)ip * kMaxQ + d];
+        gcnt[ip] = dcnt[(size_t)ip * kMaxQ + 1];
+        g2cnt[ip] = dcnt[(size_t)ip * kMaxQ + 2];
         bcnt[ip] = nbb;
-        cnt[ip] = nin[ip] - na - nbb;
+        cnt[ip] = nin[ip] - gcnt[ip] - g2cnt[ip] - bcnt[ip];
     }
     std::vector<int64_t>().swap(dcnt);
     std::vector<int64_t> farptr(n + 1, 0);
@@ -226,7 +230,7 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int dc_in, 
     const int64_t nf = farptr[n], nA = HA.bp[nblk], nB = HB.bp[nblk];
     T.nnz_far = nf;
     T.nnz_near = 0;
-    for (int64_t i = 0; i < n; i++) T.nnz_near += acnt[i] + bcnt[i];
+    for (int64_t i = 0; i < n; i++) T.nnz_near += bcnt[i] + gcnt[i] + g2cnt[i];
     T.nnz_strict = F.nnz() - (upper ? n : 0);
 
     auto upload_near = [&](const NearHost& H, int64_t total, NearDev& D) {
@@ -244,6 +248,7 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int dc_in, 
     upload_near(HA, nA, T.nearA);
     upload_near(HB, nB, T.nearB);
     SSB_CUDA(cudaMalloc(&T.dinv, std::max<int64_t>(1, nblk * PK) * sizeof(double2)));
+    SSB_CUDA(cudaMalloc(&T.G, std::max<int64_t>(1, nblk * 2 * B * B) * sizeof(double2)));
     SSB_CUDA(cudaMalloc(&T.rfar, std::max<int64_t>(1, nblk * B) * sizeof(double2)));
     SSB_CUDA(cudaMalloc(&T.fflag, std::max<int64_t>(1, nblk) * sizeof(uint32_t)));
     SSB_CUDA(cudaMalloc(&T.xfront, sizeof(unsigned long long)));
@@ -309,14 +314,16 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int dc_in, 
         r0 = r1;
     }
 
-    // dense diagonal blocks -> explicit inverses, in block chunks
-    const int64_t kBlkChunk = std::max<int64_t>(1, ((int64_t)1 << 27) / (PK * 16));
-    std::vector<double2> ibuf;
+    // dense diagonal blocks -> explicit inverses D_k^{-1}, and Gd_k = D_k^{-1} T_{k,k-d} for
+    // d = 1, 2 (column-major, G1 then G2 per block), in block chunks
+    const int64_t kBlkChunk = std::max<int64_t>(1, ((int64_t)1 << 27) / ((PK + 2 * (int64_t)B * B) * 16));
+    std::vector<double2> ibuf, gbuf;
     for (int64_t k0 = 0; k0 < nblk; k0 += kBlkChunk) {
         const int64_t k1 = std::min(nblk, k0 + kBlkChunk);
         ibuf.assign((k1 - k0) * PK, make_double2(0.0, 0.0));
+        gbuf.assign((k1 - k0) * 2 * B * B, make_double2(0.0, 0.0));
         parallel_for(k1 - k0, threads, [&](int64_t lo, int64_t hi) {
-            std::vector<double2> D((size_t)B * B), X((size_t)B * B), inv(B);
+            std::vector<double2> D((size_t)B * B), X((size_t)B * B), inv(B), N1((size_t)B * B);
             for (int64_t k = k0 + lo; k < k0 + hi; k++) {
                 std::fill(D.begin(), D.end(), make_double2(0.0, 0.0));
                 const int64_t kb = k * B;
@@ -354,9 +361,41 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int dc_in, 
                     const int64_t cs = (int64_t)j * B - ((int64_t)j * (j - 1)) / 2;
                     for (int i = j; i < B; i++) out[cs + (i - j)] = X[(size_t)i * B + j];
                 }
+                // Nd = T_{k,k-d}: the distance-d entries of the block's rows; Gd = X Nd.  Row
+                // layout (ascending column): far | list B | d = 2 | d = 1 | in-block
+                for (int d = 1; d <= 2; d++) {
+                    if (k < d) continue;
+                    std::fill(N1.begin(), N1.end(), make_double2(0.0, 0.0));
+                    const int64_t kbd = (k - d) * B;
+                    bool any = false;
+                    for (int r = 0; r < B; r++) {
+                        const int64_t ip = kb + r;
+                        if (ip >= n) continue;
+                        int64_t q0, q1;
+                        row_range(ip, q0, q1);
+                        const int64_t t1 = d == 1 ? nin[ip] : nin[ip] - gcnt[ip];
+                        const int64_t t0 = t1 - (d == 1 ? gcnt[ip] : g2cnt[ip]);
+                        for (int64_t t = t0; t < t1; t++) {
+                            const int64_t q = entry(q0, q1, t);
+                            N1[(size_t)r * B + (kcol(q) - kbd)] = F.val[q];
+                            any = true;
+                        }
+                    }
+                    if (!any) continue;
+                    double2* g = &gbuf[((size_t)(k - k0) * 2 + (d - 1)) * B * B];
+                    for (int j = 0; j < B; j++)
+                        for (int i = 0; i < B; i++) {
+                            double2 acc = make_double2(0.0, 0.0);
+                            for (int m = 0; m <= i; m++)
+                                acc = cadd(acc, cmul(X[(size_t)i * B + m], N1[(size_t)m * B + j]));
+                            g[(size_t)j * B + i] = acc;
+                        }
+                }
             }
         }, 4);
         SSB_CUDA(cudaMemcpy(T.dinv + k0 * PK, ibuf.data(), (k1 - k0) * PK * sizeof(double2), cudaMemcpyHostToDevice));
+        SSB_CUDA(cudaMemcpy(T.G + k0 * 2 * B * B, gbuf.data(), (k1 - k0) * 2 * B * B * sizeof(double2),
+                            cudaMemcpyHostToDevice));
     }
     SSB_CUDA(cudaStreamSynchronize(s));
     block_trsv_prepare(T);

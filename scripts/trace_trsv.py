@@ -31,7 +31,8 @@ def main():
         pb.ss_debug_trace_trsv(s.handle, which, x.data_ptr(), y.data_ptr())   # warm
         tr = pb.ss_debug_trace_trsv(s.handle, which, x.data_ptr(), y.data_ptr()).astype(np.int64)
         t0 = tr[:, 0].min()
-        tr = tr - t0
+        for c in (0, 1, 3, 4, 5, 7):   # slots 2, 6 are clock64 intervals
+            tr[:, c] = tr[:, c] - t0
         rel = tr[1:, :]
         prev = tr[:-1, 5]
         done_prev = tr[:-1, 3]
@@ -40,12 +41,12 @@ def main():
             "blocks": int(tr.shape[0]),
             "total_us": float(tr[:, 3].max() / 1e3),
             "step_ns": med(tr[1:, 3] - tr[:-1, 3]),
-            "chain_wait_ns": med(rel[:, 0] - done_prev),
-            "nearA_ns": med(tr[:, 6] - tr[:, 0]),
-            "pbuf_wait_and_bar_ns": med(tr[:, 1] - tr[:, 6]),
-            "matvec_ns": med(rel[:, 2] - rel[:, 1]),
-            "store_ns": med(rel[:, 3] - rel[:, 2]),
-            "lieutenant_start_minus_chain_start_ns": med(tr[:, 7] - tr[:, 0]),
+            "chain_wait_for_y_ns": med(rel[:, 0] - done_prev),
+            "chain_work_ns": med(tr[:, 3] - tr[:, 0]),
+            "chain_gemv_cycles": med(tr[:, 2] + t0 * 0),
+            "chain_publish_cycles": med(tr[:, 6] + t0 * 0),
+            "y_done_minus_chain_prev_done_ns": med(rel[:, 1] - done_prev),
+            "lieutenant_start_minus_chain_prev_done_ns": med(rel[:, 7] - done_prev),
             "helper_publish_minus_prev_done_ns": med(rel[:, 4] - done_prev),
             "chain_waited_on_helpers_frac": float(np.mean(rel[:, 5] > done_prev)),
             "first_blocks": tr[:3].tolist(),
