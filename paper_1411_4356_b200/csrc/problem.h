@@ -48,7 +48,7 @@ struct HostCSR {
 // L as is, U reversed i' = n-1-i so that both are lower triangular; blocks of B rows).
 // near entries per block staged in shared memory by trsv.cu: list A (chain SM) and list B
 // (lieutenant SM); two stages of each must fit next to the inverse blocks in 227 KB
-constexpr int near_cap_a(int B) { return B <= 32 ? 1024 : 1024; }
+constexpr int near_cap_a(int B) { return B * B; }   // a source block has B columns: never exceeded
 constexpr int near_cap_b(int B) { return B <= 32 ? 4096 : 3072; }
 
 // one near list on the device (see setup.cpp::build_block_tri)

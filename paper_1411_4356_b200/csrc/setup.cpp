@@ -163,21 +163,22 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int dc_in, 
             nin[ip] = c;
         }
     });
-    // Split of the entries left of block k by source distance d (trsv.cu v6):
+    // Split of the entries left of block k by source distance d (trsv.cu v7):
     //   d = 1, 2       -> G1_k = D_k^{-1} T_{k,k-1}, G2_k = D_k^{-1} T_{k,k-2} (dense B x B;
-    //                     the chain warp and the t warp of the chain CTA)
-    //   3 <= d < Q_k   -> list B (the lieutenant CTAs of the chain's cluster)
+    //                     the chain team of the chain CTA)
+    //   d = 3          -> list A (the y warps of the chain CTA)
+    //   4 <= d < Q_k   -> list B (the lieutenant CTAs of the chain's cluster)
     //   d >= Q_k       -> far (the helper CTAs)
-    // Q_k is the largest Q <= Qmax (>= 3) whose list B fits its shared-memory stage.
-    const int qmax = std::max(3, std::min(kMaxQ, q_max));
+    // Q_k is the largest Q <= Qmax (>= 4) whose lists fit their shared-memory stages.
+    const int qmax = std::max(4, std::min(kMaxQ, q_max));
     std::vector<int> qk(nblk, qmax);
     parallel_for(nblk, threads, [&](int64_t lo, int64_t hi) {
         for (int64_t k = lo; k < hi; k++) {
             int q = qmax;
-            for (; q > 3; q--) {
+            for (; q > 4; q--) {
                 int64_t cb = 0;
                 for (int64_t ip = k * B; ip < std::min(n, (k + 1) * B); ip++)
-                    for (int d = 3; d < q; d++) cb += dcnt[(size_t)ip * kMaxQ + d];
+                    for (int d = 4; d < q; d++) cb += dcnt[(size_t)ip * kMaxQ + d];
                 if (cb <= near_cap_b(B)) break;
             }
             qk[k] = q;
@@ -186,17 +187,23 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int dc_in, 
     int qmin = qmax;
     for (int64_t k = 0; k < nblk; k++) qmin = std::min(qmin, qk[k]);
     T.Q = qmin;
-    T.Dc = 3;
-    // per row: far / list A (unused: 0) / list B / G1 / G2 entries
-    std::vector<int64_t> cnt(n), acnt(n, 0), bcnt(n), gcnt(n), g2cnt(n);
+    T.Dc = 4;
+    // per row: far / list A / list B / G1 / G2 entries; list A of a block must fit too
+    std::vector<int64_t> cnt(n), acnt(n), bcnt(n), gcnt(n), g2cnt(n);
     for (int64_t ip = 0; ip < n; ip++) {
         const int q = qk[ip / B];
         int64_t nbb = 0;
-        for (int d = 3; d < q; d++) nbb += dcnt[(size_t)ip * kMaxQ + d];
+        for (int d = 4; d < q; d++) nbb += dcnt[(size_t)ip * kMaxQ + d];
         gcnt[ip] = dcnt[(size_t)ip * kMaxQ + 1];
         g2cnt[ip] = dcnt[(size_t)ip * kMaxQ + 2];
+        acnt[ip] = dcnt[(size_t)ip * kMaxQ + 3];
         bcnt[ip] = nbb;
-        cnt[ip] = nin[ip] - gcnt[ip] - g2cnt[ip] - bcnt[ip];
+        cnt[ip] = nin[ip] - gcnt[ip] - g2cnt[ip] - acnt[ip] - bcnt[ip];
+    }
+    for (int64_t k = 0; k < nblk; k++) {
+        int64_t ca = 0;
+        for (int64_t ip = k * B; ip < std::min(n, (k + 1) * B); ip++) ca += acnt[ip];
+        SSB_CHECK(ca <= near_cap_a(B), SS_ERR_ARG, "block substitution: distance-3 list of a block exceeds its stage");
     }
     std::vector<int64_t>().swap(dcnt);
     std::vector<int64_t> farptr(n + 1, 0);

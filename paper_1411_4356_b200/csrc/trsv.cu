@@ -106,7 +106,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 constexpr int kTrace = 8;   // stamps per block when tracing (include/ss_b200.h)
-constexpr int kProducerSleep = 32, kPublisherSleep = 32;   // back-off of the polling warps (ns)
+constexpr int kProducerSleep = 32, kPublisherSleep = 16;   // back-off of the polling warps (ns)
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -137,10 +137,14 @@ struct Cfg {
     static constexpr int kLt = kCluster - 1;
     static constexpr int kCompute = 256;              // compute threads (8 warps)
     static constexpr int kNT = kCompute + 64;         // + producer warp + publisher warp
-    // chain CTA warp roles, placed for the SMSP arbiter (highest warp id first): SMSP 0 =
-    // producer (0), publisher (4), CHAIN (8); SMSP 1 = y (1), y (5), t (9); SMSPs 2, 3 = y.
-    static constexpr int kYWarps = 6;
-    static constexpr int kWProducerChain = 0, kWPublisher = 4, kWChain = 8, kWT = 9;
+    // chain CTA warp roles, placed for the SMSP arbiter (highest warp id first): the chain
+    // team = warps 6, 7, 8, 9 (the highest id on each SMSP), y = warps 2 .. 5, producer 0,
+    // publisher 1.
+    static constexpr int kTeam = 4, kTeamW0 = 6;
+    static constexpr int kYWarps = 4, kYW0 = 2;
+    static constexpr int kWProducerChain = 0, kWPublisher = 1;
+    static constexpr int kSlice = B / kTeam;          // columns of G per team warp
+    static constexpr int kCapA = near_cap_a(B);
     static constexpr int kFarWarps = kCompute / 32;   // helper warps streaming the far part
     static constexpr int kRPW = B / kFarWarps;        // far rows per helper warp
     static constexpr int kGrp = kRPW < 4 ? kRPW : 4;
@@ -155,10 +159,13 @@ struct Cfg {
     static constexpr int kNloc = B + 4;               // padded per-block row pointers (int32)
 
     static constexpr int kTPRl = 8;                   // lieutenants: threads per row
-    // chain stage: D_k^{-1} | G1_k | G2_k | r_k
+    // chain stage: D_k^{-1} | G1_k | G2_k | list A (d = 3) columns | values | row pointers | r_k
     static constexpr size_t kOffInv = 0;
     static constexpr size_t kOffG = kOffInv + (size_t)kPK * 16;
-    static constexpr size_t kOffRfar = kOffG + (size_t)2 * B * B * 16;
+    static constexpr size_t kOffAcol = kOffG + (size_t)2 * B * B * 16;
+    static constexpr size_t kOffAval = kOffAcol + (size_t)kCapA * 4;
+    static constexpr size_t kOffAloc = kOffAval + (size_t)kCapA * 16;
+    static constexpr size_t kOffRfar = kOffAloc + (size_t)kNloc * 4;
     static constexpr size_t kChainStage = kOffRfar + (size_t)B * 16;
     // lieutenant stage: list B columns | list B values | list B row pointers
     static constexpr size_t kOffBcol = 0;
@@ -170,11 +177,13 @@ struct Cfg {
         kChainStage * kStages > kLtStage * kLtStages ? kChainStage * kStages : kLtStage * kLtStages;
     static constexpr size_t kOffRing = kStageRegion;
     static constexpr size_t kOffR = kOffRing + (size_t)kRing * B * 16;
-    static constexpr size_t kOffPart = kOffR + (size_t)B * 16;
-    static constexpr size_t kOffPbuf = kOffPart + (size_t)kSegs * B * 16;
+    static constexpr size_t kOffPart = kOffR + (size_t)2 * B * 16;
+    static constexpr int kTPRy = kYWarps * 32 / B;     // y warps: threads per row of list A
+    static constexpr int kPartRows = kSegs > kTPRy ? kSegs : kTPRy;
+    static constexpr size_t kOffPbuf = kOffPart + (size_t)kPartRows * B * 16;
     static constexpr size_t kOffYbuf = kOffPbuf + (size_t)kPbuf * B * 16;
-    static constexpr size_t kOffTbuf = kOffYbuf + (size_t)kYbuf * B * 16;
-    static constexpr size_t kOffRowP = kOffTbuf + (size_t)kYbuf * B * 16;
+    static constexpr size_t kOffTpart = kOffYbuf + (size_t)kYbuf * B * 16;   // [2][kTeam][B] partials
+    static constexpr size_t kOffRowP = kOffTpart + (size_t)2 * kTeam * B * 16;
     static constexpr size_t kOffRowL = kOffRowP + (size_t)B * 8;
     static constexpr size_t kOffBar = kOffRowL + (size_t)B * 4;
     // mbarriers: full/empty per stage, xbar (lieutenant: x block landed), pbar (chain:
@@ -185,14 +194,13 @@ struct Cfg {
     static constexpr size_t kOffPbar = kOffXbar + 8 * kRing;
     static constexpr size_t kOffYfull = kOffPbar + 8 * kPbuf;
     static constexpr size_t kOffYempty = kOffYfull + 8 * kYbuf;
-    static constexpr size_t kOffTfull = kOffYempty + 8 * kYbuf;
-    static constexpr size_t kOffTempty = kOffTfull + 8 * kYbuf;
-    static constexpr size_t kOffInts = kOffTempty + 8 * kYbuf;
+    static constexpr size_t kOffPready = kOffYempty + 8 * kYbuf;
+    static constexpr size_t kOffInts = kOffPready + 8 * 2;
     static constexpr size_t kSmem = kOffInts + 64;
     static_assert(B == 32, "the chain warp holds one row per lane");
     static_assert(kCompute % B == 0 && B % kFarWarps == 0 && kRPW % kGrp == 0, "layout");
     static_assert(kChainStage % 16 == 0 && kLtStage % 16 == 0 && kOffG % 16 == 0 && kOffRfar % 16 == 0 &&
-                      kOffBval % 16 == 0 && kOffBloc % 16 == 0,
+                      kOffAval % 16 == 0 && kOffAloc % 16 == 0 && kOffBval % 16 == 0 && kOffBloc % 16 == 0,
                   "TMA alignment");
     static_assert(kSmem <= 232448, "shared memory");
 };
@@ -284,9 +292,8 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
     uint64_t* pbar = reinterpret_cast<uint64_t*>(smem + C::kOffPbar);
     uint64_t* yfull = reinterpret_cast<uint64_t*>(smem + C::kOffYfull);
     uint64_t* yempty = reinterpret_cast<uint64_t*>(smem + C::kOffYempty);
-    uint64_t* tfull = reinterpret_cast<uint64_t*>(smem + C::kOffTfull);
-    uint64_t* tempty = reinterpret_cast<uint64_t*>(smem + C::kOffTempty);
-    double2* tbuf = reinterpret_cast<double2*>(smem + C::kOffTbuf);
+    double2* tpart = reinterpret_cast<double2*>(smem + C::kOffTpart);
+    uint64_t* pready = reinterpret_cast<uint64_t*>(smem + C::kOffPready);
     int* sDone = reinterpret_cast<int*>(smem + C::kOffInts);   // chain: blocks of x done
     int* sF = sDone + 1;                                          // helpers: frontier view
     int* sLock = sDone + 2;
@@ -307,16 +314,15 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
     if (tid == 0) {
         for (int s = 0; s < C::kStages; s++) {
             mbar_init(full + s, 1);
-            mbar_init(empty + s, chain ? 3 : 1);   // chain CTA: y warps, t warp and chain warp release
+            mbar_init(empty + s, chain ? 2 + C::kTeam : 1);   // chain CTA: the y team's 2 warps + each team warp
         }
         for (int j = 0; j < C::kRing; j++) mbar_init(xbar + j, 1);
         for (int j = 0; j < C::kPbuf; j++) mbar_init(pbar + j, 1);
         for (int j = 0; j < C::kYbuf; j++) {
-            mbar_init(yfull + j, 1);
-            mbar_init(yempty + j, 1);
-            mbar_init(tfull + j, 1);
-            mbar_init(tempty + j, 1);
+            mbar_init(yfull + j, 2);
+            mbar_init(yempty + j, C::kTeam);
         }
+        for (int j = 0; j < 2; j++) mbar_init(pready + j, C::kTeam);
         *sDone = 0;
         *sF = 0;
         *sLock = 0;
@@ -340,9 +346,13 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                         while (ld_acquire(a.fflag + k) != epoch) __nanosleep(kProducerSleep);
                         if (trace) trace[(int64_t)k * kTrace + 5] = gtime();
                         fence_proxy_async();   // r_k (generic-proxy stores of a helper) -> TMA reads
-                        mbar_expect_tx(full + s, (uint32_t)(C::kPK * 16 + 2 * B * B * 16 + B * 16));
+                        const uint32_t nb = stage_near(nullptr, nullptr, nullptr, a.nbpA, a.ncolA, a.nvalA,
+                                                       a.nlocA, k, C::kNloc, full + s, false);
+                        mbar_expect_tx(full + s, (uint32_t)(C::kPK * 16 + 2 * B * B * 16 + B * 16) + nb);
                         bulk_g2s(st + C::kOffInv, a.dinv + (int64_t)k * C::kPK, C::kPK * 16, full + s);
                         bulk_g2s(st + C::kOffG, a.G + (int64_t)k * 2 * B * B, 2 * B * B * 16, full + s);
+                        stage_near(st + C::kOffAcol, st + C::kOffAval, st + C::kOffAloc, a.nbpA, a.ncolA, a.nvalA,
+                                   a.nlocA, k, C::kNloc, full + s, true);
                         bulk_g2s(st + C::kOffRfar, a.rfar + (int64_t)k * B, B * 16, full + s);
                     } else {
                         const uint32_t nb = stage_near(nullptr, nullptr, nullptr, a.nbpB, a.ncolB, a.nvalB,
@@ -353,159 +363,187 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     }
                 }
             }
-        } else if (chain ? warp == C::kWPublisher : warp == C::kCompute / 32 + 1) {
-            // ------------------------------------------------ publisher (chain CTA only)
-            if (chain) {
-                int published = 0;
-                while (published < nblk) {
-                    const int d = ld_acq_cta(sDone);
-                    if (d > published) {
-                        for (int j = published; j < d; j++) {
-                            const int64_t i = (int64_t)j * B + lane;
-                            if (i < n) {
-                                const double2 v = ring[i & kRingMask];
-                                const int64_t pi = phys(i);
-                                x[pi] = v;
-                                if (a.operm) out[a.operm[pi]] = v;
-                            }
-                        }
-                        __syncwarp();
-                        if (lane == 0) {
-                            st_release64(a.xfront, ((unsigned long long)epoch << 32) | (unsigned)d);
-                            st_rel_cta(sPub, d);
-                        }
-                        published = d;
-                    } else {
-                        __nanosleep(kPublisherSleep);
-                    }
-                }
-            }
-        } else if (chain && warp == C::kWChain) {
-            // ------------------------------------------------ the chain warp: x_k = y_k - G_k x_{k-1}
+        } else if (chain && warp == C::kWPublisher) {
+            // ------------------------------------------------ publisher: x blocks from the ring to
+            // global memory (and through the iLUTP column permutation to the output), to the
+            // lieutenants' rings (st.async, completing their mbarrier transactions), then the
+            // gpu-scope frontier word
             uint32_t peer_ring[C::kLt], peer_xbar[C::kLt];
 #pragma unroll
             for (int l = 0; l < C::kLt; l++) {
                 peer_ring[l] = mapa(smem_u32(ring), (uint32_t)(l + 1));
                 peer_xbar[l] = mapa(smem_u32(xbar), (uint32_t)(l + 1));
             }
-            double2 xprev = make_double2(0.0, 0.0);
-            double2 g[B];   // G1_k, column j in g[j] (lane = row), prefetched a step ahead
-            auto load_g1 = [&](int k) {
+            int published = 0;
+            while (published < nblk) {
+                const int d = ld_acq_cta(sDone);
+                if (d > published) {
+                    for (int j = published; j < d; j++) {
+                        const int64_t i = (int64_t)j * B + lane;
+                        const double2 v = ring[i & kRingMask];
+#pragma unroll
+                        for (int l = 0; l < C::kLt; l++)
+                            st_async2(peer_ring[l] + (uint32_t)((i & kRingMask) * 16), v,
+                                      peer_xbar[l] + (uint32_t)((j % C::kRing) * 8));
+                        if (i < n) {
+                            const int64_t pi = phys(i);
+                            x[pi] = v;
+                            if (a.operm) out[a.operm[pi]] = v;
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) {
+                        st_release64(a.xfront, ((unsigned long long)epoch << 32) | (unsigned)d);
+                        st_rel_cta(sPub, d);
+                    }
+                    published = d;
+                } else {
+                    __nanosleep(kPublisherSleep);
+                }
+            }
+        } else if (chain && warp >= C::kTeamW0) {
+            // ------------------------------------------------ chain team (4 warps):
+            // x_k = y_k - sum_w [ G1_k[:, slice_w] x_{k-1}[slice_w] + G2_k[:, slice_w] x_{k-2}[slice_w] ]
+            // Warp w owns 8 columns; the G2 term of block k+1 (which needs x_{k-1}) is formed
+            // in step k's tail.  One named barrier per step; every team warp then reduces the
+            // partials itself, so all of them hold x_k (lane = row) for the next step.
+            const int tw = warp - C::kTeamW0;
+            const int j0 = tw * C::kSlice;
+            double2 g1[C::kSlice], g2[C::kSlice];
+            auto load_g = [&](int k) {   // G1_k (stage k) and G2_{k+1} (stage k+1); release stage k
                 const int s = k % C::kStages;
                 mbar_wait(full + s, (uint32_t)((k / C::kStages) & 1));
-                const double2* G = reinterpret_cast<const double2*>(smem + C::kChainStage * s + C::kOffG);
+                const double2* G1 = reinterpret_cast<const double2*>(smem + C::kChainStage * s + C::kOffG);
 #pragma unroll
-                for (int j = 0; j < B; j++) g[j] = G[j * B + lane];
+                for (int u = 0; u < C::kSlice; u++) g1[u] = G1[(j0 + u) * B + lane];
+                if (k + 1 < nblk) {
+                    const int s1 = (k + 1) % C::kStages;
+                    mbar_wait(full + s1, (uint32_t)(((k + 1) / C::kStages) & 1));
+                    const double2* G2 =
+                        reinterpret_cast<const double2*>(smem + C::kChainStage * s1 + C::kOffG) + B * B;
+#pragma unroll
+                    for (int u = 0; u < C::kSlice; u++) g2[u] = G2[(j0 + u) * B + lane];
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + s);   // this warp is done with stage k
             };
-            if (nblk > 0) load_g1(0);
+            double2 xk = make_double2(0.0, 0.0);      // x_{k-1}[lane]
+            double2 carry = make_double2(0.0, 0.0);   // G2_k[lane, slice] x_{k-2}[slice]
+            if (nblk > 0) load_g(0);
             for (int k = 0; k < nblk; k++) {
-                const int s = k % C::kStages, yb = k % C::kYbuf;
+                const int yb = k % C::kYbuf;
+                double2 xs[C::kSlice];
+#pragma unroll
+                for (int u = 0; u < C::kSlice; u++) {
+                    xs[u].x = __shfl_sync(0xffffffffu, xk.x, j0 + u);
+                    xs[u].y = __shfl_sync(0xffffffffu, xk.y, j0 + u);
+                }
+                double2 p0 = carry, p1 = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int u = 0; u < C::kSlice; u += 2) {
+                    p0 = cfma(p0, g1[u], xs[u]);
+                    p1 = cfma(p1, g1[u + 1], xs[u + 1]);
+                }
+                tpart[((k & 1) * C::kTeam + tw) * B + lane] = cadd(p0, p1);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(pready + (k & 1));   // this warp's partial is in tpart
+                // tail (off the critical path): G2_{k+1} x_{k-1} for the next step
+                double2 c0 = make_double2(0.0, 0.0), c1 = make_double2(0.0, 0.0);
+                if (k + 1 < nblk) {
+#pragma unroll
+                    for (int u = 0; u < C::kSlice; u += 2) {
+                        c0 = cfma(c0, g2[u], xs[u]);
+                        c1 = cfma(c1, g2[u + 1], xs[u + 1]);
+                    }
+                }
+                carry = cadd(c0, c1);
+                if (k + 1 < nblk) load_g(k + 1);   // next G slices: overlaps the barrier wait
                 mbar_wait(yfull + yb, (uint32_t)((k / C::kYbuf) & 1));   // y_k
-                mbar_wait(tfull + yb, (uint32_t)((k / C::kYbuf) & 1));   // t_k = G2_k x_{k-2}
-                if (trace && lane == 0) trace[(int64_t)k * kTrace + 0] = gtime();
-                long long c0 = clock64();
-                double2 acc[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0),
-                                  make_double2(0.0, 0.0)};
+                mbar_wait(pready + (k & 1), (uint32_t)((k >> 1) & 1));   // all team partials
+                if (trace && tw == 0 && lane == 0) trace[(int64_t)k * kTrace + 0] = gtime();
+                double2 sum = tpart[((k & 1) * C::kTeam + 0) * B + lane];
 #pragma unroll
-                for (int j = 0; j < B; j++) {
-                    double2 xj;
-                    xj.x = __shfl_sync(0xffffffffu, xprev.x, j);
-                    xj.y = __shfl_sync(0xffffffffu, xprev.y, j);
-                    acc[j & 3] = cfma(acc[j & 3], g[j], xj);
-                }
-                const double2 y = ybuf[yb * B + lane], t = tbuf[yb * B + lane];
-                const double2 v = csub(csub(y, t), cadd(cadd(acc[0], acc[1]), cadd(acc[2], acc[3])));
-                long long c1;
-                asm volatile("mov.u64 %0, %%clock64;" : "=l"(c1) : "d"(v.x), "d"(v.y));
-                // the ring slot of block k held block k-8: the publisher must have copied it
-                if (k >= C::kRing)
-                    while (ld_acq_cta(sPub) < k - C::kRing + 1) {
-                    }
-                const int64_t i = (int64_t)k * B + lane;
-                ring[i & kRingMask] = v;
-#pragma unroll
-                for (int l = 0; l < C::kLt; l++)
-                    st_async2(peer_ring[l] + (uint32_t)((i & kRingMask) * 16), v,
-                              peer_xbar[l] + (uint32_t)((k % C::kRing) * 8));
-                xprev = v;
+                for (int w = 1; w < C::kTeam; w++) sum = cadd(sum, tpart[((k & 1) * C::kTeam + w) * B + lane]);
+                xk = csub(ybuf[yb * B + lane], sum);
                 __syncwarp();
-                const long long c2 = clock64();
-                if (lane == 0) {
-                    if (trace) {
-                        trace[(int64_t)k * kTrace + 2] = c1 - c0;
-                        trace[(int64_t)k * kTrace + 6] = c2 - c1;
+                if (lane == 0) mbar_arrive(yempty + yb);
+                if (tw == 0) {
+                    // the ring slot of block k held block k-8: the publisher must have copied it
+                    if (k >= C::kRing)
+                        while (ld_acq_cta(sPub) < k - C::kRing + 1) {
+                        }
+                    ring[((int64_t)k * B + lane) & kRingMask] = xk;
+                    __syncwarp();
+                    if (lane == 0) {
+                        st_rel_cta(sDone, k + 1);   // publisher, y warps
+                        if (trace) trace[(int64_t)k * kTrace + 3] = gtime();
                     }
-                    mbar_arrive(yempty + yb);
-                    mbar_arrive(tempty + yb);
-                    mbar_arrive(empty + s);
-                    st_rel_cta(sDone, k + 1);   // the publisher copies x_k to global memory
-                    if (trace) trace[(int64_t)k * kTrace + 3] = gtime();
-                }
-                if (k + 1 < nblk) load_g1(k + 1);   // off the critical path until y_{k+1} is ready
-            }
-        } else if (chain && warp == C::kWT) {
-            // ------------------------------------------------ t warp: t_k = G2_k x_{k-2}
-            double2 g[B];
-            for (int k = 0; k < nblk; k++) {
-                const int s = k % C::kStages, tb = k % C::kYbuf;
-                mbar_wait(full + s, (uint32_t)((k / C::kStages) & 1));
-                const double2* G2 = reinterpret_cast<const double2*>(smem + C::kChainStage * s + C::kOffG) + B * B;
-#pragma unroll
-                for (int j = 0; j < B; j++) g[j] = G2[j * B + lane];
-                double2 acc[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0),
-                                  make_double2(0.0, 0.0)};
-                if (k >= 2) {
-                    while (ld_acq_cta(sDone) < k - 1) {
-                    }   // x_{k-2} is in the ring
-                    const double2 xo = ring[((int64_t)(k - 2) * B + lane) & kRingMask];
-#pragma unroll
-                    for (int j = 0; j < B; j++) {
-                        double2 xj;
-                        xj.x = __shfl_sync(0xffffffffu, xo.x, j);
-                        xj.y = __shfl_sync(0xffffffffu, xo.y, j);
-                        acc[j & 3] = cfma(acc[j & 3], g[j], xj);
-                    }
-                }
-                if (k >= C::kYbuf) mbar_wait(tempty + tb, (uint32_t)((k / C::kYbuf - 1) & 1));
-                tbuf[tb * B + lane] = cadd(cadd(acc[0], acc[1]), cadd(acc[2], acc[3]));
-                __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(tfull + tb);
-                    mbar_arrive(empty + s);
                 }
             }
-        } else if (chain) {
-            // ------------------------------------------------ y warps: y_k = D_k^{-1} (r_k - partials)
-            const int yw = warp - 1 - (warp > 4 ? 1 : 0);   // warps 1, 2, 3, 5, 6, 7 -> 0 .. 5
-            const int yt = yw * 32 + lane;                   // 0 .. 191
-            constexpr int kYT = C::kYWarps * 32;
-            double2* sR = reinterpret_cast<double2*>(smem + C::kOffR);
-            double2* sPart = reinterpret_cast<double2*>(smem + C::kOffPart);
-            for (int k = 0; k < nblk; k++) {
+        } else if (chain && warp >= C::kYW0) {
+            // ------------------------------------------------ y warps: y_k = D_k^{-1} (r_k - A3_k x_{k-3} - partials)
+            // 4 threads per row (r = row, q = column class): D_k^{-1}[r, j], j = q mod 4,
+            // j <= r, lives in registers; one named barrier per block (the residual vector).
+            // two y teams of 2 warps take the even / odd blocks (each has two chain steps)
+            const int yteam = (warp - C::kYW0) >> 1;           // 0: even blocks, 1: odd blocks
+            const int yt = ((warp - C::kYW0) & 1) * 32 + lane;   // 0 .. 63
+            constexpr int kYT = 64;
+            constexpr int kQ = kYT / B;                     // 2 threads per row
+            const int r = yt / kQ, q = yt % kQ;
+            double2* sR = reinterpret_cast<double2*>(smem + C::kOffR) + yteam * B;   // [2][B]
+            for (int k = yteam; k < nblk; k += 2) {
                 const int s = k % C::kStages, yb = k % C::kYbuf, pk = k % C::kPbuf;
                 unsigned char* st = smem + C::kChainStage * s;
                 mbar_wait(full + s, (uint32_t)((k / C::kStages) & 1));
-                if (yt < B) {
-                    if (yt == 0) mbar_expect_tx(pbar + pk, (uint32_t)(B * 16));
-                    mbar_wait(pbar + pk, (uint32_t)((k / C::kPbuf) & 1));   // lieutenants' partials
-                    const double2* sRfar = reinterpret_cast<const double2*>(st + C::kOffRfar);
-                    sR[yt] = csub(sRfar[yt], pbuf[pk * B + yt]);
+                const double2* sInv = reinterpret_cast<const double2*>(st + C::kOffInv);
+                double2 dv[B / kQ];
+#pragma unroll
+                for (int t = 0; t < B / kQ; t++) {
+                    const int j = q + kQ * t;
+                    dv[t] = j <= r ? sInv[j * B - (j * (j - 1)) / 2 + (r - j)] : make_double2(0.0, 0.0);
                 }
-                bar_named(2, kYT);
-                trimv::matvec_tiles<B, C::kCW, C::kYWarps>(reinterpret_cast<const double2*>(st + C::kOffInv), sR,
-                                                            sPart, yw, lane);
-                bar_named(2, kYT);
-                if (yt < B) {
-                    const double2 yv = trimv::sum_row<B, C::kCW>(sPart, yt);
+                const double2 rf = reinterpret_cast<const double2*>(st + C::kOffRfar)[r];
+                // list A: source distance 3 (x_{k-3}, in the ring once the team has done it)
+                if (k >= 3)
+                    while (ld_acq_cta(sDone) < k - 2) {
+                    }
+                if (trace && yt == 0) trace[(int64_t)k * kTrace + 2] = gtime();
+                double2 acc = near_part<B, kQ>(reinterpret_cast<const int32_t*>(st + C::kOffAloc),
+                                               reinterpret_cast<const int32_t*>(st + C::kOffAcol),
+                                               reinterpret_cast<const double2*>(st + C::kOffAval), ring, r, q);
+#pragma unroll
+                for (int o = 1; o < kQ; o <<= 1) {
+                    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+                    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+                }
+                if (yt == 0) mbar_expect_tx(pbar + pk, (uint32_t)(B * 16));
+                mbar_wait(pbar + pk, (uint32_t)((k / C::kPbuf) & 1));   // lieutenants' partials
+                if (trace && yt == 0) trace[(int64_t)k * kTrace + 6] = gtime();
+                if (q == 0) sR[r] = csub(csub(rf, acc), pbuf[pk * B + r]);
+                bar_named(2 + yteam * 2, kYT);   // the team's residual vector is complete
+                double2 y0 = make_double2(0.0, 0.0), y1 = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int t = 0; t < B / kQ; t += 2) {
+                    y0 = cfma(y0, dv[t], sR[q + kQ * t]);
+                    y1 = cfma(y1, dv[t + 1], sR[q + kQ * (t + 1)]);
+                }
+                double2 yv = cadd(y0, y1);
+#pragma unroll
+                for (int o = 1; o < kQ; o <<= 1) {
+                    yv.x += __shfl_xor_sync(0xffffffffu, yv.x, o);
+                    yv.y += __shfl_xor_sync(0xffffffffu, yv.y, o);
+                }
+                if (q == 0) {
                     if (k >= C::kYbuf) mbar_wait(yempty + yb, (uint32_t)((k / C::kYbuf - 1) & 1));
-                    ybuf[yb * B + yt] = yv;
+                    ybuf[yb * B + r] = yv;
                 }
-                bar_named(2, kYT);
-                if (yt == 0) {
-                    mbar_arrive(yfull + yb);
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(yfull + yb);   // one arrival per y warp of the team (its 16 rows)
                     mbar_arrive(empty + s);
-                    if (trace) trace[(int64_t)k * kTrace + 1] = gtime();
+                    if (trace && yt == 0) trace[(int64_t)k * kTrace + 1] = gtime();
                 }
+                bar_named(2 + yteam * 2, kYT);   // sR is reused by the team's next block
             }
         } else if (!chain) {
             // ------------------------------------------------ lieutenants: list B partial sums
@@ -515,39 +553,41 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
             int xseen = 0;   // x blocks < xseen have landed in the ring
             const int r = l + C::kLt * (tid / C::kTPRl), q = tid % C::kTPRl;
             const bool rowok = r < B;
-            for (int k = 0; k < nblk; k++) {
-                const int s = k % nst;
-                unsigned char* st = smem + stsz * s;
-                mbar_wait(full + s, (uint32_t)((k / nst) & 1));
-                // list B of block k reads x of blocks <= k - 3: consume their arrivals in
-                // order (each xbar phase exactly once)
-                for (; xseen <= k - 3; xseen++) {
+            if (warp < C::kCompute / 32) {
+                for (int k = 0; k < nblk; k++) {
+                    const int s = k % nst;
+                    unsigned char* st = smem + stsz * s;
+                    mbar_wait(full + s, (uint32_t)((k / nst) & 1));
+                    // list B of block k reads x of blocks <= k - 4: consume their arrivals in
+                    // order (each xbar phase exactly once)
+                    for (; xseen <= k - 4; xseen++) {
+                        const int j = xseen % C::kRing;
+                        if (tid == 0) mbar_expect_tx(xbar + j, (uint32_t)(B * 16));
+                        mbar_wait(xbar + j, (uint32_t)((xseen / C::kRing) & 1));
+                    }
+                    if (trace && tid == 0 && l == 0) trace[(int64_t)k * kTrace + 7] = gtime();
+                    double2 acc = make_double2(0.0, 0.0);
+                    if (rowok)
+                        acc = near_part<B, C::kTPRl>(reinterpret_cast<const int32_t*>(st + C::kOffBloc),
+                                                     reinterpret_cast<const int32_t*>(st + C::kOffBcol),
+                                                     reinterpret_cast<const double2*>(st + C::kOffBval), ring, r, q);
+#pragma unroll
+                    for (int o = 1; o < C::kTPRl; o <<= 1) {
+                        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+                        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+                    }
+                    if (rowok && q == 0) {
+                        const int pk = k % C::kPbuf;
+                        st_async2(peer_pbuf + (uint32_t)((pk * B + r) * 16), acc, peer_pbar + (uint32_t)(pk * 8));
+                    }
+                    bar_named(2, C::kCompute);
+                    if (tid == 0) mbar_arrive(empty + s);
+                }
+                for (; xseen < nblk; xseen++) {   // drain the remaining arrivals before leaving
                     const int j = xseen % C::kRing;
                     if (tid == 0) mbar_expect_tx(xbar + j, (uint32_t)(B * 16));
                     mbar_wait(xbar + j, (uint32_t)((xseen / C::kRing) & 1));
                 }
-                if (trace && tid == 0 && l == 0) trace[(int64_t)k * kTrace + 7] = gtime();
-                double2 acc = make_double2(0.0, 0.0);
-                if (rowok)
-                    acc = near_part<B, C::kTPRl>(reinterpret_cast<const int32_t*>(st + C::kOffBloc),
-                                                 reinterpret_cast<const int32_t*>(st + C::kOffBcol),
-                                                 reinterpret_cast<const double2*>(st + C::kOffBval), ring, r, q);
-#pragma unroll
-                for (int o = 1; o < C::kTPRl; o <<= 1) {
-                    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-                    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
-                }
-                if (rowok && q == 0) {
-                    const int pk = k % C::kPbuf;
-                    st_async2(peer_pbuf + (uint32_t)((pk * B + r) * 16), acc, peer_pbar + (uint32_t)(pk * 8));
-                }
-                bar_named(2, C::kCompute);
-                if (tid == 0) mbar_arrive(empty + s);
-            }
-            for (; xseen < nblk; xseen++) {   // drain the remaining arrivals before leaving
-                const int j = xseen % C::kRing;
-                if (tid == 0) mbar_expect_tx(xbar + j, (uint32_t)(B * 16));
-                mbar_wait(xbar + j, (uint32_t)((xseen / C::kRing) & 1));
             }
         }
         // no CTA of the cluster leaves while a peer may still access its shared memory

@@ -31,8 +31,7 @@ def main():
         pb.ss_debug_trace_trsv(s.handle, which, x.data_ptr(), y.data_ptr())   # warm
         tr = pb.ss_debug_trace_trsv(s.handle, which, x.data_ptr(), y.data_ptr()).astype(np.int64)
         t0 = tr[:, 0].min()
-        for c in (0, 1, 3, 4, 5, 7):   # slots 2, 6 are clock64 intervals
-            tr[:, c] = tr[:, c] - t0
+        tr = tr - t0
         rel = tr[1:, :]
         prev = tr[:-1, 5]
         done_prev = tr[:-1, 3]
@@ -41,12 +40,15 @@ def main():
             "blocks": int(tr.shape[0]),
             "total_us": float(tr[:, 3].max() / 1e3),
             "step_ns": med(tr[1:, 3] - tr[:-1, 3]),
-            "chain_wait_for_y_ns": med(rel[:, 0] - done_prev),
-            "chain_work_ns": med(tr[:, 3] - tr[:, 0]),
-            "chain_gemv_cycles": med(tr[:, 2] + t0 * 0),
-            "chain_publish_cycles": med(tr[:, 6] + t0 * 0),
-            "y_done_minus_chain_prev_done_ns": med(rel[:, 1] - done_prev),
-            "lieutenant_start_minus_chain_prev_done_ns": med(rel[:, 7] - done_prev),
+            "team_barrier_minus_prev_done_ns": med(rel[:, 0] - done_prev),
+            "team_reduce_publish_ns": med(tr[:, 3] - tr[:, 0]),
+            "y_done_minus_prev_done_ns": med(rel[:, 1] - done_prev),
+            "y_late_frac": float(np.mean(rel[:, 1] > rel[:, 0])),
+            "y_start_minus_prev_done_ns": med(rel[:, 2] - done_prev),
+            "y_near_and_pbar_ns": med(tr[:, 6] - tr[:, 2]),
+            "y_rest_ns": med(tr[:, 1] - tr[:, 6]),
+            "y_start_minus_prev_y_done_ns": med(tr[1:, 2] - tr[:-1, 1]),
+            "lieutenant_start_minus_prev_done_ns": med(rel[:, 7] - done_prev),
             "helper_publish_minus_prev_done_ns": med(rel[:, 4] - done_prev),
             "chain_waited_on_helpers_frac": float(np.mean(rel[:, 5] > done_prev)),
             "first_blocks": tr[:3].tolist(),
