@@ -206,11 +206,14 @@ def ss_precond(h, which: int, x_dev_ptr: int, y_dev_ptr: int):
     _check(load().ss_precond(h, int(which), P(x_dev_ptr), P(y_dev_ptr)))
 
 
+TRACE_STAMPS = 16   # SS_TRACE_STAMPS
+
+
 def ss_debug_trace_trsv(h, which: int, x_dev_ptr: int, y_dev_ptr: int) -> np.ndarray:
-    """Per-block globaltimer stamps (ns), shape (nblk, 8); see include/ss_b200.h."""
+    """Per-block globaltimer stamps (ns), shape (nblk, TRACE_STAMPS); see include/ss_b200.h."""
     nb = ctypes.c_int64()
     _check(load().ss_debug_trace_trsv(h, int(which), P(x_dev_ptr), P(y_dev_ptr), None, ctypes.byref(nb)))
-    tr = np.empty((nb.value, 8), np.uint64)
+    tr = np.empty((nb.value, TRACE_STAMPS), np.uint64)
     _check(load().ss_debug_trace_trsv(h, int(which), P(x_dev_ptr), P(y_dev_ptr), tr.ctypes.data, ctypes.byref(nb)))
     return tr
 

@@ -280,10 +280,11 @@ int ss_debug_trace_trsv(ss_problem* h, int32_t which, const void* x_dev, void* y
     *nblk_out = T.nblk;
     if (!host_trace) return SS_OK;
     unsigned long long* d = nullptr;
-    SSB_CUDA(cudaMalloc(&d, T.nblk * 8 * sizeof(unsigned long long)));
+    SSB_CUDA(cudaMalloc(&d, T.nblk * SS_TRACE_STAMPS * sizeof(unsigned long long)));
     try {
+        SSB_CUDA(cudaMemsetAsync(d, 0, T.nblk * SS_TRACE_STAMPS * sizeof(unsigned long long), P.stream));
         block_trsv(T, (const double2*)x_dev, (double2*)y_dev, P.stream, d);
-        SSB_CUDA(cudaMemcpyAsync(host_trace, d, T.nblk * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+        SSB_CUDA(cudaMemcpyAsync(host_trace, d, T.nblk * SS_TRACE_STAMPS * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                  P.stream));
         SSB_CUDA(cudaStreamSynchronize(P.stream));
     } catch (...) {

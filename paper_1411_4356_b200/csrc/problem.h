@@ -46,17 +46,24 @@ struct HostCSR {
 
 // Triangular factor on the device in the block layout of trsv.cu (kernel index space:
 // L as is, U reversed i' = n-1-i so that both are lower triangular; blocks of B rows).
-// near entries per block staged in shared memory by trsv.cu: list A (chain SM) and list B
-// (lieutenant SM); two stages of each must fit next to the inverse blocks in 227 KB
-constexpr int near_cap_a(int B) { return B * B; }   // a source block has B columns: never exceeded
-constexpr int near_cap_b(int B) { return B <= 32 ? 4096 : 3072; }
+// Source-distance split of the entries left of block k (d = k - source block):
+//   d = 1 .. kDense    -> dense G_d = D_k^{-1} T_{k,k-d} (the chain teams)
+//   d = kDense + 1     -> list A, staged per block in the chain CTA (the A warp)
+//   kDense+1 < d < Q_k -> list B, staged per lieutenant CTA and block
+//   d >= Q_k           -> far part (helper CTAs)
+constexpr int kDense = 2;
+constexpr int near_cap_a(int B) { return B <= 32 ? 960 : B * B; }   // list A entries per block
+constexpr int near_cap_b(int B) { return B <= 32 ? 2048 : 1536; }   // per lieutenant and block
+constexpr int kLieutenants = 3;   // list B CTAs of a chain cluster (trsv.cu)
+constexpr int near_nloc(int B) { return 2 * (B + 4); }   // per list: row starts | late-part starts
 
 // one near list on the device (see setup.cpp::build_block_tri)
 struct NearDev {
     int64_t* bp = nullptr;    // [nblk+1] start of block k's list (multiple of 4 entries)
     int32_t* col = nullptr;   // kernel-space columns, rows in order
     double2* val = nullptr;
-    int32_t* loc = nullptr;   // [nblk][B+4] row pointers relative to bp[k]
+    int32_t* loc = nullptr;   // [list][2(B+4)] row starts, then starts of each row's d = kDense+1
+                              // entries (the late part), relative to bp[list]
     void release() {
         cudaFree(bp);
         cudaFree(col);
@@ -72,26 +79,25 @@ struct TriArgs {
     const int64_t* farptr;    // [n+1] entries of row i' with source block <= k-Q_k (k = i'/B)
     const int32_t* fcol;      //       kernel-space columns, ascending within a row
     const double2* fval;
-    const int64_t* nbpA;      // near list A: source blocks k-Dc+1 .. k-1 (chain SM)
+    const int64_t* nbpA;      // near list A: [nblk+1] (chain CTA)
     const int32_t* ncolA;
     const double2* nvalA;
     const int32_t* nlocA;
-    const int64_t* nbpB;      // near list B: source blocks k-Q_k+1 .. k-Dc (lieutenant SM)
+    const int64_t* nbpB;      // near list B: [nblk*kLieutenants+1], list of (block k, lieutenant l) at k*kLt+l
     const int32_t* ncolB;
     const double2* nvalB;
     const int32_t* nlocB;
     const double2* dinv;      // [nblk][B(B+1)/2] inverse diagonal blocks, packed lower, column-major
-    const double2* G;         // [nblk][2][B*B] D_k^{-1} T_{k,k-d}, d = 1, 2, column-major
+    const double2* G;         // [nblk][kDense][B*B] D_k^{-1} T_{k,k-d}, d = 1 .. kDense, column-major
     double2* rfar;            // [nblk*B] b - (far part), written by the helper CTAs
     const int64_t* operm;     // [n] output permutation out[operm[i]] = x[i] (ILUTP columns), or null
     uint32_t* fflag;          // [nblk] "rfar of block k is ready" (value = launch epoch)
     unsigned long long* xfront;   // (epoch << 32) | number of blocks of x published
-    int32_t Dc;
 };
 
 struct DevBlockTri {
     int64_t n = 0, nblk = 0, nnz_far = 0, nnz_near = 0, nnz_strict = 0;
-    int B = 0, rev = 0, nt = 0, Q = 0, Dc = 2;   // rows per block, reversed (U), threads, windows
+    int B = 0, rev = 0, nt = 0, Q = 0;   // rows per block, reversed (U), threads, smallest Q_k
     int64_t* farptr = nullptr;
     int32_t* fcol = nullptr;
     double2* fval = nullptr;
@@ -107,10 +113,9 @@ struct DevBlockTri {
     int grid = 0;
     int64_t nlev = 0;   // row-level dependency levels (diagnostic)
     TriArgs args() const {
-        return TriArgs{n,           nblk,        rev,         B,          farptr,       fcol,        fval,
-                       nearA.bp,    nearA.col,   nearA.val,   nearA.loc,  nearB.bp,     nearB.col,   nearB.val,
-                       nearB.loc,   dinv,        G,           rfar,       operm,        fflag,       xfront,
-                       Dc};
+        return TriArgs{n,         nblk,      rev,       B,         farptr,    fcol,  fval, nearA.bp,
+                       nearA.col, nearA.val, nearA.loc, nearB.bp,  nearB.col, nearB.val, nearB.loc,
+                       dinv,      G,         rfar,      operm,     fflag,     xfront};
     }
     void release() {
         cudaFree(farptr);

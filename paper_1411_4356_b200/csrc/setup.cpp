@@ -121,7 +121,12 @@ int64_t count_levels(const HostCSR& F, bool upper) {
 // pointers relative to the block start); the in-block entries and the diagonal (1 for
 // L, u_ii for U) form the dense block D_k, whose inverse is stored packed (lower,
 // column-major; column j = rows j..B-1).  The last block is padded with identity rows.
-void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int dc_in, int threads, DevBlockTri& T,
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+
+void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads, DevBlockTri& T,
                      cudaStream_t s) {
     T.release();
     const int64_t n = F.n;
@@ -144,7 +149,7 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int dc_in, 
     // per row: entries per source distance d = k - source block (d = 1 .. kMaxQ-1; d >= kMaxQ
     // counted together); the near window Q (near = d < Q, far = d >= Q) is the largest
     // Q <= Qmax whose per-block near lists fit the shared-memory stage (kNearCap)
-    constexpr int kMaxQ = 8;
+    constexpr int kMaxQ = 16;
     std::vector<int64_t> dcnt((size_t)n * kMaxQ, 0);   // [row][d], d = 0 means ">= kMaxQ"
     std::vector<int64_t> nin(n);                        // strict entries left of the block
     parallel_for(n, threads, [&](int64_t lo, int64_t hi) {
@@ -163,23 +168,37 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int dc_in, 
             nin[ip] = c;
         }
     });
-    // Split of the entries left of block k by source distance d (trsv.cu v7):
-    //   d = 1, 2       -> G1_k = D_k^{-1} T_{k,k-1}, G2_k = D_k^{-1} T_{k,k-2} (dense B x B;
-    //                     the chain team of the chain CTA)
-    //   d = 3          -> list A (the y warps of the chain CTA)
-    //   4 <= d < Q_k   -> list B (the lieutenant CTAs of the chain's cluster)
-    //   d >= Q_k       -> far (the helper CTAs)
-    // Q_k is the largest Q <= Qmax (>= 4) whose lists fit their shared-memory stages.
-    const int qmax = std::max(4, std::min(kMaxQ, q_max));
+    // Split of the entries left of block k by source distance d (problem.h, trsv.cu):
+    //   d = 1 .. kDense       -> dense G_d = D_k^{-1} T_{k,k-d} (the chain teams)
+    //   d = kDA = kDense+1    -> list A (the A warp of the chain CTA, one thread per row)
+    //   kDA < d < Q_k         -> list B (the lieutenant CTAs of the chain's cluster; lieutenant
+    //                            l holds the rows r = l mod kLieutenants of the block); the
+    //                            d = kDA+1 entries of each row (the last ones) form its late part
+    //   d >= Q_k              -> far (the helper CTAs)
+    // Q_k is the largest Q <= Qmax (>= kDA+1) whose per-lieutenant lists fit their stages; a
+    // block whose list A overflows its stage takes Q_k = kDA (d >= kDA to the helpers).
+    // A row's entries in ascending column: far | list B (late part last) | list A | G_kDense ..
+    // G_1 | block.
+    constexpr int kDA = kDense + 1, kD1 = kDA + 1;
+    const int qmax = std::max(kD1, std::min(kMaxQ, q_max));
+    const int capa = std::min(near_cap_a(B), env_int("SSB_TRSV_CAPA", near_cap_a(B)));   // (tests lower it)
     std::vector<int> qk(nblk, qmax);
     parallel_for(nblk, threads, [&](int64_t lo, int64_t hi) {
         for (int64_t k = lo; k < hi; k++) {
+            int64_t ca = 0;
+            for (int64_t ip = k * B; ip < std::min(n, (k + 1) * B); ip++) ca += dcnt[(size_t)ip * kMaxQ + kDA];
+            if (ca + 3 > capa) {
+                qk[k] = kDA;
+                continue;
+            }
             int q = qmax;
-            for (; q > 4; q--) {
-                int64_t cb = 0;
+            for (; q > kD1; q--) {
+                int64_t cb[kLieutenants] = {};
                 for (int64_t ip = k * B; ip < std::min(n, (k + 1) * B); ip++)
-                    for (int d = 4; d < q; d++) cb += dcnt[(size_t)ip * kMaxQ + d];
-                if (cb <= near_cap_b(B)) break;
+                    for (int d = kD1; d < q; d++) cb[(ip - k * B) % kLieutenants] += dcnt[(size_t)ip * kMaxQ + d];
+                bool fit = true;
+                for (int l = 0; l < kLieutenants; l++) fit = fit && cb[l] + 3 <= near_cap_b(B);
+                if (fit) break;
             }
             qk[k] = q;
         }
@@ -187,66 +206,68 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int dc_in, 
     int qmin = qmax;
     for (int64_t k = 0; k < nblk; k++) qmin = std::min(qmin, qk[k]);
     T.Q = qmin;
-    T.Dc = 4;
-    // per row: far / list A / list B / G1 / G2 entries; list A of a block must fit too
-    std::vector<int64_t> cnt(n), acnt(n), bcnt(n), gcnt(n), g2cnt(n);
+    // per row: far / list B (its late part) / list A / dense G_d entries
+    std::vector<int64_t> cnt(n), acnt(n), bcnt(n), blate(n), gcnt((size_t)n * kDense);
     for (int64_t ip = 0; ip < n; ip++) {
         const int q = qk[ip / B];
-        int64_t nbb = 0;
-        for (int d = 4; d < q; d++) nbb += dcnt[(size_t)ip * kMaxQ + d];
-        gcnt[ip] = dcnt[(size_t)ip * kMaxQ + 1];
-        g2cnt[ip] = dcnt[(size_t)ip * kMaxQ + 2];
-        acnt[ip] = dcnt[(size_t)ip * kMaxQ + 3];
+        int64_t nbb = 0, ng = 0;
+        for (int d = kD1; d < q; d++) nbb += dcnt[(size_t)ip * kMaxQ + d];
+        for (int d = 1; d <= kDense; d++) ng += (gcnt[(size_t)ip * kDense + d - 1] = dcnt[(size_t)ip * kMaxQ + d]);
+        acnt[ip] = q > kDA ? dcnt[(size_t)ip * kMaxQ + kDA] : 0;
         bcnt[ip] = nbb;
-        cnt[ip] = nin[ip] - gcnt[ip] - g2cnt[ip] - acnt[ip] - bcnt[ip];
-    }
-    for (int64_t k = 0; k < nblk; k++) {
-        int64_t ca = 0;
-        for (int64_t ip = k * B; ip < std::min(n, (k + 1) * B); ip++) ca += acnt[ip];
-        SSB_CHECK(ca <= near_cap_a(B), SS_ERR_ARG, "block substitution: distance-3 list of a block exceeds its stage");
+        blate[ip] = q > kD1 ? dcnt[(size_t)ip * kMaxQ + kD1] : 0;
+        cnt[ip] = nin[ip] - ng - acnt[ip] - nbb;
     }
     std::vector<int64_t>().swap(dcnt);
     std::vector<int64_t> farptr(n + 1, 0);
     for (int64_t i = 0; i < n; i++) farptr[i + 1] = farptr[i] + cnt[i];
-    // a near list: per block a padded start, per row a local pointer
+    // near lists: per (block, group) a padded start, per row a local pointer and the local
+    // start of its late part (list A: one group, no late part; list B: a group per lieutenant)
     struct NearHost {
-        std::vector<int64_t> bp, row;   // block starts [nblk+1], global row starts [n]
-        std::vector<int32_t> loc;       // [nblk][B+4]
+        std::vector<int64_t> bp, row;   // list starts [nblk*G+1], global row starts [n]
+        std::vector<int32_t> loc;       // [nblk*G][2(B+4)]
     };
-    auto layout = [&](const std::vector<int64_t>& c, NearHost& H) {
-        H.bp.assign(nblk + 1, 0);
+    const int NL = near_nloc(B);
+    auto layout = [&](const std::vector<int64_t>& c, const std::vector<int64_t>* late, int G, NearHost& H) {
+        H.bp.assign(nblk * G + 1, 0);
         H.row.assign(n, 0);
-        H.loc.assign((size_t)nblk * (B + 4), 0);
-        for (int64_t k = 0; k < nblk; k++) {
-            int64_t off = 0;
-            for (int r = 0; r < B; r++) {
-                const int64_t ip = k * B + r;
-                H.loc[(size_t)k * (B + 4) + r] = (int32_t)off;
-                if (ip < n) {
-                    H.row[ip] = H.bp[k] + off;
-                    off += c[ip];
+        H.loc.assign((size_t)nblk * G * NL, 0);
+        for (int64_t k = 0; k < nblk; k++)
+            for (int g = 0; g < G; g++) {
+                const int64_t idx = k * G + g;
+                int32_t* loc = &H.loc[(size_t)idx * NL];
+                int64_t off = 0;
+                for (int r = 0; r < B; r++) {
+                    const int64_t ip = k * B + r;
+                    loc[r] = (int32_t)off;
+                    loc[B + 4 + r] = (int32_t)off;
+                    if (ip < n && r % G == g) {
+                        H.row[ip] = H.bp[idx] + off;
+                        off += c[ip];
+                        loc[B + 4 + r] = (int32_t)(off - (late ? (*late)[ip] : 0));
+                    }
                 }
+                for (int r = B; r < B + 4; r++) loc[r] = loc[B + 4 + r] = (int32_t)off;
+                H.bp[idx + 1] = H.bp[idx] + ((off + 3) & ~(int64_t)3);
             }
-            for (int r = B; r < B + 4; r++) H.loc[(size_t)k * (B + 4) + r] = (int32_t)off;
-            H.bp[k + 1] = H.bp[k] + ((off + 3) & ~(int64_t)3);
-        }
     };
+    constexpr int G = kLieutenants;
     NearHost HA, HB;
-    layout(acnt, HA);
-    layout(bcnt, HB);
-    const int64_t nf = farptr[n], nA = HA.bp[nblk], nB = HB.bp[nblk];
+    layout(acnt, nullptr, 1, HA);
+    layout(bcnt, &blate, G, HB);
+    const int64_t nf = farptr[n], nA = HA.bp[nblk], nB = HB.bp[nblk * G];
     T.nnz_far = nf;
     T.nnz_near = 0;
-    for (int64_t i = 0; i < n; i++) T.nnz_near += bcnt[i] + gcnt[i] + g2cnt[i];
+    for (int64_t i = 0; i < n; i++) T.nnz_near += nin[i] - cnt[i];
     T.nnz_strict = F.nnz() - (upper ? n : 0);
 
     auto upload_near = [&](const NearHost& H, int64_t total, NearDev& D) {
-        SSB_CUDA(cudaMalloc(&D.bp, (nblk + 1) * sizeof(int64_t)));
+        SSB_CUDA(cudaMalloc(&D.bp, H.bp.size() * sizeof(int64_t)));
         SSB_CUDA(cudaMalloc(&D.col, std::max<int64_t>(4, total) * sizeof(int32_t)));
         SSB_CUDA(cudaMalloc(&D.val, std::max<int64_t>(4, total) * sizeof(double2)));
         SSB_CUDA(cudaMalloc(&D.loc, H.loc.size() * sizeof(int32_t)));
         SSB_CUDA(cudaMemsetAsync(D.col, 0, std::max<int64_t>(4, total) * sizeof(int32_t), s));   // padding
-        SSB_CUDA(cudaMemcpyAsync(D.bp, H.bp.data(), (nblk + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        SSB_CUDA(cudaMemcpyAsync(D.bp, H.bp.data(), H.bp.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s));
         SSB_CUDA(cudaMemcpyAsync(D.loc, H.loc.data(), H.loc.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     };
     SSB_CUDA(cudaMalloc(&T.farptr, (n + 1) * sizeof(int64_t)));
@@ -255,7 +276,7 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int dc_in, 
     upload_near(HA, nA, T.nearA);
     upload_near(HB, nB, T.nearB);
     SSB_CUDA(cudaMalloc(&T.dinv, std::max<int64_t>(1, nblk * PK) * sizeof(double2)));
-    SSB_CUDA(cudaMalloc(&T.G, std::max<int64_t>(1, nblk * 2 * B * B) * sizeof(double2)));
+    SSB_CUDA(cudaMalloc(&T.G, std::max<int64_t>(1, nblk * kDense * B * B) * sizeof(double2)));
     SSB_CUDA(cudaMalloc(&T.rfar, std::max<int64_t>(1, nblk * B) * sizeof(double2)));
     SSB_CUDA(cudaMalloc(&T.fflag, std::max<int64_t>(1, nblk) * sizeof(uint32_t)));
     SSB_CUDA(cudaMalloc(&T.xfront, sizeof(unsigned long long)));
@@ -264,19 +285,21 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int dc_in, 
     SSB_CUDA(cudaMemcpyAsync(T.farptr, farptr.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
     SSB_CUDA(cudaStreamSynchronize(s));
 
-    // entries, in row chunks of ~2^26 (bounded host staging); the rows of a chunk map to
-    // contiguous ranges of the far CSR and of both near lists
+    // entries, in block chunks of ~2^26 (bounded host staging); the rows of a chunk of
+    // blocks map to contiguous ranges of the far CSR and of list B
     const int64_t kChunk = (int64_t)1 << 26;
     std::vector<int32_t> fc, ac, bc;
     std::vector<double2> fv, av, bv;
-    for (int64_t r0 = 0; r0 < n;) {
-        int64_t r1 = r0 + 1;
-        while (r1 < n && (farptr[r1 + 1] - farptr[r0]) + (HA.row[r1] + acnt[r1] - HA.row[r0]) +
-                                 (HB.row[r1] + bcnt[r1] - HB.row[r0]) <= kChunk)
-            r1++;
+    auto frow = [&](int64_t k) { return farptr[std::min(n, k * B)]; };
+    for (int64_t k0 = 0; k0 < nblk;) {
+        int64_t k1 = k0 + 1;
+        while (k1 < nblk && (frow(k1 + 1) - frow(k0)) + (HA.bp[k1 + 1] - HA.bp[k0]) +
+                                    (HB.bp[(k1 + 1) * G] - HB.bp[k0 * G]) <= kChunk)
+            k1++;
+        const int64_t r0 = k0 * B, r1 = std::min(n, k1 * B);
         const int64_t fb = farptr[r0], flen = farptr[r1] - fb;
-        const int64_t ab = HA.row[r0], alen = HA.row[r1 - 1] + acnt[r1 - 1] - ab;
-        const int64_t bb = HB.row[r0], blen = HB.row[r1 - 1] + bcnt[r1 - 1] - bb;
+        const int64_t ab = HA.bp[k0], alen = HA.bp[k1] - ab;
+        const int64_t bb = HB.bp[k0 * G], blen = HB.bp[k1 * G] - bb;
         fc.resize(flen);
         fv.resize(flen);
         ac.assign(alen, 0);
@@ -287,7 +310,7 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int dc_in, 
             for (int64_t ip = r0 + lo; ip < r0 + hi; ip++) {
                 int64_t q0, q1;
                 row_range(ip, q0, q1);
-                // row layout (ascending column = descending distance): far | list B | list A | block
+                // row layout (ascending column = descending distance): far | list B | list A | dense | block
                 int64_t t = 0;
                 for (int64_t u = 0; u < cnt[ip]; u++, t++) {
                     const int64_t q = entry(q0, q1, t);
@@ -318,17 +341,17 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int dc_in, 
             SSB_CUDA(cudaMemcpy(T.nearB.col + bb, bc.data(), blen * sizeof(int32_t), cudaMemcpyHostToDevice));
             SSB_CUDA(cudaMemcpy(T.nearB.val + bb, bv.data(), blen * sizeof(double2), cudaMemcpyHostToDevice));
         }
-        r0 = r1;
+        k0 = k1;
     }
 
     // dense diagonal blocks -> explicit inverses D_k^{-1}, and Gd_k = D_k^{-1} T_{k,k-d} for
-    // d = 1, 2 (column-major, G1 then G2 per block), in block chunks
-    const int64_t kBlkChunk = std::max<int64_t>(1, ((int64_t)1 << 27) / ((PK + 2 * (int64_t)B * B) * 16));
+    // d = 1 .. kDense (column-major, G1 first per block), in block chunks
+    const int64_t kBlkChunk = std::max<int64_t>(1, ((int64_t)1 << 27) / ((PK + kDense * (int64_t)B * B) * 16));
     std::vector<double2> ibuf, gbuf;
     for (int64_t k0 = 0; k0 < nblk; k0 += kBlkChunk) {
         const int64_t k1 = std::min(nblk, k0 + kBlkChunk);
         ibuf.assign((k1 - k0) * PK, make_double2(0.0, 0.0));
-        gbuf.assign((k1 - k0) * 2 * B * B, make_double2(0.0, 0.0));
+        gbuf.assign((k1 - k0) * kDense * B * B, make_double2(0.0, 0.0));
         parallel_for(k1 - k0, threads, [&](int64_t lo, int64_t hi) {
             std::vector<double2> D((size_t)B * B), X((size_t)B * B), inv(B), N1((size_t)B * B);
             for (int64_t k = k0 + lo; k < k0 + hi; k++) {
@@ -369,8 +392,8 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int dc_in, 
                     for (int i = j; i < B; i++) out[cs + (i - j)] = X[(size_t)i * B + j];
                 }
                 // Nd = T_{k,k-d}: the distance-d entries of the block's rows; Gd = X Nd.  Row
-                // layout (ascending column): far | list B | d = 2 | d = 1 | in-block
-                for (int d = 1; d <= 2; d++) {
+                // layout (ascending column): far | list B | d = kDense | .. | d = 1 | in-block
+                for (int d = 1; d <= kDense; d++) {
                     if (k < d) continue;
                     std::fill(N1.begin(), N1.end(), make_double2(0.0, 0.0));
                     const int64_t kbd = (k - d) * B;
@@ -380,8 +403,9 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int dc_in, 
                         if (ip >= n) continue;
                         int64_t q0, q1;
                         row_range(ip, q0, q1);
-                        const int64_t t1 = d == 1 ? nin[ip] : nin[ip] - gcnt[ip];
-                        const int64_t t0 = t1 - (d == 1 ? gcnt[ip] : g2cnt[ip]);
+                        int64_t t1 = nin[ip];
+                        for (int e = 1; e < d; e++) t1 -= gcnt[(size_t)ip * kDense + e - 1];
+                        const int64_t t0 = t1 - gcnt[(size_t)ip * kDense + d - 1];
                         for (int64_t t = t0; t < t1; t++) {
                             const int64_t q = entry(q0, q1, t);
                             N1[(size_t)r * B + (kcol(q) - kbd)] = F.val[q];
@@ -389,7 +413,8 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int dc_in, 
                         }
                     }
                     if (!any) continue;
-                    double2* g = &gbuf[((size_t)(k - k0) * 2 + (d - 1)) * B * B];
+                    // column-major (the chain teams: lane = row, a warp per 8 columns)
+                    double2* g = &gbuf[((size_t)(k - k0) * kDense + (d - 1)) * B * B];
                     for (int j = 0; j < B; j++)
                         for (int i = 0; i < B; i++) {
                             double2 acc = make_double2(0.0, 0.0);
@@ -401,7 +426,7 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int dc_in, 
             }
         }, 4);
         SSB_CUDA(cudaMemcpy(T.dinv + k0 * PK, ibuf.data(), (k1 - k0) * PK * sizeof(double2), cudaMemcpyHostToDevice));
-        SSB_CUDA(cudaMemcpy(T.G + k0 * 2 * B * B, gbuf.data(), (k1 - k0) * 2 * B * B * sizeof(double2),
+        SSB_CUDA(cudaMemcpy(T.G + k0 * kDense * B * B, gbuf.data(), (k1 - k0) * kDense * B * B * sizeof(double2),
                             cudaMemcpyHostToDevice));
     }
     SSB_CUDA(cudaStreamSynchronize(s));
@@ -409,10 +434,6 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int dc_in, 
 }
 
 // Tuning knobs of the block substitution: rows per block and CTA size.
-int env_int(const char* name, int dflt) {
-    const char* e = std::getenv(name);
-    return e ? std::atoi(e) : dflt;
-}
 
 }  // namespace
 
@@ -436,16 +457,15 @@ void setup_problem(Problem& P, double drop_tol, double fill_factor, double permt
     SSB_CUDA(cudaMemcpyAsync(P.d_perm, P.perm.data(), P.n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
     if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
     const int B = env_int("SSB_TRSV_B", 32);
-    const int QMAX = env_int("SSB_TRSV_Q", 8);
-    const int DC = env_int("SSB_TRSV_DC", 2);
+    const int QMAX = env_int("SSB_TRSV_Q", 16);
     int64_t levL = 0, levU = 0;
     std::thread lev([&] {
         levL = count_levels(P.hL, false);
         levU = count_levels(P.hU, true);
     });
     try {
-        build_block_tri(P.hL, false, B, QMAX, DC, threads, P.L, s);
-        build_block_tri(P.hU, true, B, QMAX, DC, threads, P.U, s);
+        build_block_tri(P.hL, false, B, QMAX, threads, P.L, s);
+        build_block_tri(P.hU, true, B, QMAX, threads, P.U, s);
         bool identity = true;
         for (int64_t q = 0; q < P.n && identity; q++) identity = P.colperm[q] == q;
         if (!identity) {   // ILUTP exchanged columns: the U substitution scatters x = Pi y

@@ -38,7 +38,6 @@
 // the spin waits cannot deadlock.  Every reduction has a fixed order: the result is
 // deterministic for given (B, Q).
 #include "problem.h"
-#include "trimv.cuh"
 
 namespace ssb {
 
@@ -83,6 +82,12 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
+// arrive on a peer CTA's mbarrier (shared::cluster address), adding bytes to its expected
+// transaction count
+__device__ __forceinline__ void mbar_arrive_expect_tx_remote(uint32_t addr, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(addr), "r"(bytes)
+                 : "memory");
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -92,6 +97,19 @@ __device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t 
             smem_u32(smem)),
         "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {   // non-blocking
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
@@ -105,8 +123,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
-constexpr int kTrace = 8;   // stamps per block when tracing (include/ss_b200.h)
-constexpr int kProducerSleep = 32, kPublisherSleep = 16;   // back-off of the polling warps (ns)
+constexpr int kTrace = SS_TRACE_STAMPS;   // stamps per block when tracing (include/ss_b200.h)
+// STAMP: the ss_debug_trace_trsv stamps (%globaltimer).  Built with -DSSB_TEAM_PROF instead,
+// TPROF stamps clock64() at sub-steps of the chain team's warp 0 (scripts/trace_trsv.py --team).
+#ifdef SSB_TEAM_PROF
+#define STAMP(k, i) ((void)0)
+#define TPROF(k, i) \
+    if (trace && tw == 0 && lane == 0) trace[(int64_t)(k) * kTrace + (i)] = clock64()
+#else
+#define STAMP(k, i) (trace[(int64_t)(k) * kTrace + (i)] = gtime())
+#define TPROF(k, i) ((void)0)
+#endif
+constexpr int kProducerSleep = 32;   // back-off of the producer polling a helper flag (ns)
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -133,74 +161,95 @@ __device__ __forceinline__ void cluster_sync() {
 // ------------------------------------------------------------------ configuration
 template <int B>
 struct Cfg {
-    static constexpr int kCluster = 4;                // chain + 3 lieutenants
-    static constexpr int kLt = kCluster - 1;
+    static constexpr int kLt = kLieutenants;
+    static constexpr int kCluster = 1 + kLt;          // chain + lieutenants
     static constexpr int kCompute = 256;              // compute threads (8 warps)
-    static constexpr int kNT = kCompute + 64;         // + producer warp + publisher warp
-    // chain CTA warp roles, placed for the SMSP arbiter (highest warp id first): the chain
-    // team = warps 6, 7, 8, 9 (the highest id on each SMSP), y = warps 2 .. 5, producer 0,
-    // publisher 1.
-    static constexpr int kTeam = 4, kTeamW0 = 6;
-    static constexpr int kYWarps = 4, kYW0 = 2;
-    static constexpr int kWProducerChain = 0, kWPublisher = 1;
+    static constexpr int kNT = 512;                   // chain CTA: 16 warps (roles below)
+    // chain CTA warp roles (warp w runs on SMSP w mod 4): producer 0, publisher 1, G producer
+    // 2, A warp 3 (list A), y warps 4 .. 7 (two y teams of two), chain teams A = warps 8 .. 11
+    // (even blocks) and B = 12 .. 15 (odd blocks), one warp of each team per SMSP
+    static constexpr int kTeam = 4, kTeamW0 = 8;
+    static constexpr int kYW0 = 4;
+    static constexpr int kWProducerChain = 0, kWPublisher = 1, kWGProducer = 2, kWA = 3;
+    static constexpr int kDA = kDense + 1;            // list A source distance
     static constexpr int kSlice = B / kTeam;          // columns of G per team warp
-    static constexpr int kCapA = near_cap_a(B);
     static constexpr int kFarWarps = kCompute / 32;   // helper warps streaming the far part
     static constexpr int kRPW = B / kFarWarps;        // far rows per helper warp
     static constexpr int kGrp = kRPW < 4 ? kRPW : 4;
-    static constexpr int kStages = 3;
-    static constexpr int kRing = 8;                   // x of the last 8 blocks (Q <= 8)
+    static constexpr int kGStages = 3;                // G1 | G2 ring (chain teams, a block ahead)
+    static constexpr int kSStages = 4;                // D^{-1} / r ring (y warps)
+    static constexpr int kAStages = 3;                // list A ring (A warp)
+    static constexpr int kCapA = near_cap_a(B);
+    static constexpr int kRing = 8;                   // chain CTA: x of the last 8 blocks
+    static constexpr int kRingLt = 16;                // lieutenants: x of the last 16 blocks (Q <= 16)
     static constexpr int kPbuf = 4;                   // lieutenant partial-sum slots
     static constexpr int kYbuf = 2;                   // y slots
     static constexpr int kPK = B * (B + 1) / 2;
     static constexpr int kCapB = near_cap_b(B);
-    static constexpr int kCW = 8;                     // mat-vec tile width
-    static constexpr int kSegs = B / kCW;
-    static constexpr int kNloc = B + 4;               // padded per-block row pointers (int32)
+    static constexpr int kNloc = near_nloc(B);        // per list: row starts | late-part starts
+    static constexpr int kLate = B + 4;               // offset of the late-part starts
 
+    static constexpr int kLtTeamT = kCompute / 2;     // lieutenants: two teams (even / odd blocks)
     static constexpr int kTPRl = 8;                   // lieutenants: threads per row
-    // chain stage: D_k^{-1} | G1_k | G2_k | list A (d = 3) columns | values | row pointers | r_k
+    // chain CTA: a G ring (G1_k | G2_k), an S ring (D_k^{-1} | r_k) and an A ring (list A), filled
+    // independently (G is static, r_k waits for the helpers)
+    static constexpr size_t kGStage = (size_t)2 * B * B * 16;
+    static constexpr size_t kOffSR = kGStage * kGStages;
     static constexpr size_t kOffInv = 0;
-    static constexpr size_t kOffG = kOffInv + (size_t)kPK * 16;
-    static constexpr size_t kOffAcol = kOffG + (size_t)2 * B * B * 16;
+    static constexpr size_t kOffRfar = kOffInv + (size_t)kPK * 16;
+    static constexpr size_t kSStage = kOffRfar + (size_t)B * 16;
+    static constexpr size_t kOffAR = kOffSR + kSStage * kSStages;
+    static constexpr size_t kOffAcol = 0;
     static constexpr size_t kOffAval = kOffAcol + (size_t)kCapA * 4;
     static constexpr size_t kOffAloc = kOffAval + (size_t)kCapA * 16;
-    static constexpr size_t kOffRfar = kOffAloc + (size_t)kNloc * 4;
-    static constexpr size_t kChainStage = kOffRfar + (size_t)B * 16;
-    // lieutenant stage: list B columns | list B values | list B row pointers
+    static constexpr size_t kAStage = kOffAloc + (size_t)kNloc * 4;
+    static constexpr size_t kChainRegion = kOffAR + kAStage * kAStages;
+    // lieutenant stage: list B columns | values | row pointers
     static constexpr size_t kOffBcol = 0;
     static constexpr size_t kOffBval = kOffBcol + (size_t)kCapB * 4;
     static constexpr size_t kOffBloc = kOffBval + (size_t)kCapB * 16;
     static constexpr size_t kLtStage = kOffBloc + (size_t)kNloc * 4;
-    static constexpr int kLtStages = 2;
-    static constexpr size_t kStageRegion =
-        kChainStage * kStages > kLtStage * kLtStages ? kChainStage * kStages : kLtStage * kLtStages;
+    static constexpr int kLtStages = 4;
+    static constexpr size_t kOffLtRing = kLtStage * kLtStages;   // lieutenants' x ring
+    static constexpr size_t kLtRegion = kOffLtRing + (size_t)kRingLt * B * 16;
+    static constexpr size_t kStageRegion = kChainRegion > kLtRegion ? kChainRegion : kLtRegion;
     static constexpr size_t kOffRing = kStageRegion;
     static constexpr size_t kOffR = kOffRing + (size_t)kRing * B * 16;
-    static constexpr size_t kOffPart = kOffR + (size_t)2 * B * 16;
-    static constexpr int kTPRy = kYWarps * 32 / B;     // y warps: threads per row of list A
-    static constexpr int kPartRows = kSegs > kTPRy ? kSegs : kTPRy;
-    static constexpr size_t kOffPbuf = kOffPart + (size_t)kPartRows * B * 16;
+    static constexpr size_t kOffPbuf = kOffR + (size_t)2 * B * 16;
     static constexpr size_t kOffYbuf = kOffPbuf + (size_t)kPbuf * B * 16;
-    static constexpr size_t kOffTpart = kOffYbuf + (size_t)kYbuf * B * 16;   // [2][kTeam][B] partials
-    static constexpr size_t kOffRowP = kOffTpart + (size_t)2 * kTeam * B * 16;
+    static constexpr size_t kOffTpart = kOffYbuf + (size_t)kYbuf * B * 16;   // [4][kTeam][B] partials
+    static constexpr size_t kOffXw = kOffTpart + (size_t)4 * kTeam * B * 16;   // [2 kTeam][B] own x_k
+    static constexpr size_t kOffAbuf = kOffXw + (size_t)2 * kTeam * B * 16;   // [2][B] list A products
+    static constexpr size_t kOffRowP = kOffAbuf + (size_t)2 * B * 16;
     static constexpr size_t kOffRowL = kOffRowP + (size_t)B * 8;
     static constexpr size_t kOffBar = kOffRowL + (size_t)B * 4;
-    // mbarriers: full/empty per stage, xbar (lieutenant: x block landed), pbar (chain:
-    // partial landed), yfull/yempty (y slots), then int counters
+    // mbarriers: full/empty per S stage (lieutenants: per list B stage), full/empty per G
+    // stage, xbar (lieutenant: x block landed), pbar (chain: partial landed), xfull (ring slot
+    // holds x_k), yempty (y slots), pready (team partials and y_k), then int counters
+    static constexpr int kNS = kSStages > kLtStages ? kSStages : kLtStages;
     static constexpr size_t kOffFull = kOffBar;
-    static constexpr size_t kOffEmpty = kOffFull + 8 * kStages;
-    static constexpr size_t kOffXbar = kOffEmpty + 8 * kStages;
-    static constexpr size_t kOffPbar = kOffXbar + 8 * kRing;
-    static constexpr size_t kOffYfull = kOffPbar + 8 * kPbuf;
-    static constexpr size_t kOffYempty = kOffYfull + 8 * kYbuf;
+    static constexpr size_t kOffEmpty = kOffFull + 8 * kNS;
+    static constexpr size_t kOffGfull = kOffEmpty + 8 * kNS;
+    static constexpr size_t kOffGempty = kOffGfull + 8 * kGStages;
+    static constexpr size_t kOffXbar = kOffGempty + 8 * kGStages;
+    static constexpr size_t kOffPbar = kOffXbar + 8 * kRingLt;
+    static constexpr size_t kOffXfull = kOffPbar + 8 * kPbuf;
+    static constexpr size_t kOffYempty = kOffXfull + 8 * kRing;
     static constexpr size_t kOffPready = kOffYempty + 8 * kYbuf;
-    static constexpr size_t kOffInts = kOffPready + 8 * 2;
+    static constexpr size_t kOffRfull = kOffPready + 8 * 4;
+    static constexpr size_t kOffAready = kOffRfull + 8 * kSStages;
+    static constexpr size_t kOffAempty = kOffAready + 8 * 2;
+    static constexpr size_t kOffAfull = kOffAempty + 8 * 2;   // A ring
+    static constexpr size_t kOffAslot = kOffAfull + 8 * kAStages;
+    static constexpr size_t kOffInts = kOffAslot + 8 * kAStages;
     static constexpr size_t kSmem = kOffInts + 64;
-    static_assert(B == 32, "the chain warp holds one row per lane");
+    static_assert(B == 32 && kDense == 2, "the chain teams hold one row per lane and the G1, G2 blocks");
     static_assert(kCompute % B == 0 && B % kFarWarps == 0 && kRPW % kGrp == 0, "layout");
-    static_assert(kChainStage % 16 == 0 && kLtStage % 16 == 0 && kOffG % 16 == 0 && kOffRfar % 16 == 0 &&
-                      kOffAval % 16 == 0 && kOffAloc % 16 == 0 && kOffBval % 16 == 0 && kOffBloc % 16 == 0,
+    static_assert(kTeamW0 + 2 * kTeam == kNT / 32 && kCompute / 32 + 1 <= kNT / 32, "warp roles");
+    static_assert(kTPRl * ((B + kLt - 1) / kLt) <= kLtTeamT, "lieutenant rows");
+    static_assert(kSStage % 16 == 0 && kLtStage % 16 == 0 && kOffSR % 16 == 0 && kOffRfar % 16 == 0 &&
+                      kOffAR % 16 == 0 && kAStage % 16 == 0 && kOffAval % 16 == 0 && kOffAloc % 16 == 0 &&
+                      kOffBval % 16 == 0 && kOffBloc % 16 == 0 && kOffLtRing % 16 == 0,
                   "TMA alignment");
     static_assert(kSmem <= 232448, "shared memory");
 };
@@ -232,48 +281,37 @@ __device__ __forceinline__ void helper_wait(int target, int* sF, int* sLock, con
     __syncwarp();   // every lane's later loads follow the acquire chain
 }
 
-// Near products of row r of one block's list (TPR threads per row, contiguous parts,
-// thread q of the row): returns the row sum on every thread of the row group, x read
-// from the ring.  TPR need not be a power of two; the groups must not straddle warps
-// unevenly, so the reduction goes through shared memory when TPR is not a power of two.
-template <int B, int TPR>
-__device__ __forceinline__ double2 near_part(const int32_t* loc, const int32_t* col, const double2* val,
-                                             const double2* ring, int r, int q) {
-    constexpr int kRingMask = Cfg<B>::kRing * B - 1;
-    const int lo = loc[r], hi = loc[r + 1], len = hi - lo;
-    const int e0 = lo + (q * len) / TPR, e1 = lo + ((q + 1) * len) / TPR;
-    double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
-    int e = e0;
-    for (; e + 4 <= e1; e += 4) {
-        const int c0 = col[e], c1 = col[e + 1], c2 = col[e + 2], c3 = col[e + 3];
-        const double2 v0 = val[e], v1 = val[e + 1], v2 = val[e + 2], v3 = val[e + 3];
-        const double2 x0 = ring[c0 & kRingMask], x1 = ring[c1 & kRingMask];
-        const double2 x2 = ring[c2 & kRingMask], x3 = ring[c3 & kRingMask];
-        acc = cfma(acc, v0, x0);
-        acc2 = cfma(acc2, v1, x1);
-        acc = cfma(acc, v2, x2);
-        acc2 = cfma(acc2, v3, x3);
+// Entries [lo, hi) of one row of a staged list B, interleaved over the TPR threads of the
+// row (thread q takes lo+q, lo+q+TPR, ...: the row's threads read consecutive entries),
+// x from the lieutenant's ring.  Returns this thread's share (reduced by the caller).
+template <int B, int TPR, int kRingBlocks>
+__device__ __forceinline__ double2 near_range(const int32_t* col, const double2* val, const double2* ring, int lo,
+                                              int hi, int q, double2 acc) {
+    constexpr int kRingMask = kRingBlocks * B - 1;
+    double2 acc2 = make_double2(0.0, 0.0);
+    int e = lo + q;
+    for (; e + TPR < hi; e += 2 * TPR) {
+        const int c0 = col[e], c1 = col[e + TPR];
+        const double2 v0 = val[e], v1 = val[e + TPR];
+        acc = cfma(acc, v0, ring[c0 & kRingMask]);
+        acc2 = cfma(acc2, v1, ring[c1 & kRingMask]);
     }
-    for (; e < e1; e++) acc = cfma(acc, val[e], ring[col[e] & kRingMask]);
+    if (e < hi) acc = cfma(acc, val[e], ring[col[e] & kRingMask]);
     return cadd(acc, acc2);
 }
 
-// Stage one near list block (TMA): columns (padded to 4), values, row pointers.
-__device__ __forceinline__ uint32_t stage_near(unsigned char* col_dst, unsigned char* val_dst,
-                                               unsigned char* loc_dst, const int64_t* bp, const int32_t* col,
-                                               const double2* val, const int32_t* loc, int k, int nloc,
-                                               uint64_t* bar, bool issue) {
-    const int64_t b0 = bp[k];
-    const uint32_t cnt = (uint32_t)(bp[k + 1] - b0);   // already a multiple of 4
-    const uint32_t bytes = cnt * 20 + (uint32_t)nloc * 4;
-    if (issue) {
-        if (cnt) {
-            bulk_g2s(col_dst, col + b0, cnt * 4, bar);
-            bulk_g2s(val_dst, val + b0, cnt * 16, bar);
-        }
-        bulk_g2s(loc_dst, loc + (int64_t)k * nloc, (uint32_t)nloc * 4, bar);
+// Stage list g (TMA): entries [b0, b1) (columns, values; a multiple of 4) and row pointers,
+// `extra` more bytes expected on the same barrier (one arrival).
+__device__ __forceinline__ void stage_near(unsigned char* col_dst, unsigned char* val_dst, unsigned char* loc_dst,
+                                           int64_t b0, int64_t b1, const int32_t* col, const double2* val,
+                                           const int32_t* loc, int g, int nloc, uint64_t* bar, uint32_t extra = 0) {
+    const uint32_t cnt = (uint32_t)(b1 - b0);
+    mbar_expect_tx(bar, cnt * 20 + (uint32_t)nloc * 4 + extra);
+    if (cnt) {
+        bulk_g2s(col_dst, col + b0, cnt * 4, bar);
+        bulk_g2s(val_dst, val + b0, cnt * 16, bar);
     }
-    return bytes;
+    bulk_g2s(loc_dst, loc + (int64_t)g * nloc, (uint32_t)nloc * 4, bar);
 }
 
 __device__ __forceinline__ void bar_named(int id, int nthreads) {
@@ -288,9 +326,17 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kOffFull);
     uint64_t* empty = reinterpret_cast<uint64_t*>(smem + C::kOffEmpty);
+    uint64_t* gfull = reinterpret_cast<uint64_t*>(smem + C::kOffGfull);
+    uint64_t* gempty = reinterpret_cast<uint64_t*>(smem + C::kOffGempty);
     uint64_t* xbar = reinterpret_cast<uint64_t*>(smem + C::kOffXbar);
     uint64_t* pbar = reinterpret_cast<uint64_t*>(smem + C::kOffPbar);
-    uint64_t* yfull = reinterpret_cast<uint64_t*>(smem + C::kOffYfull);
+    uint64_t* xfull = reinterpret_cast<uint64_t*>(smem + C::kOffXfull);
+    uint64_t* rfull = reinterpret_cast<uint64_t*>(smem + C::kOffRfull);   // chain: r_k staged
+    uint64_t* aready = reinterpret_cast<uint64_t*>(smem + C::kOffAready);  // chain: list A product
+    uint64_t* aempty = reinterpret_cast<uint64_t*>(smem + C::kOffAempty);
+    double2* abuf = reinterpret_cast<double2*>(smem + C::kOffAbuf);
+    uint64_t* afull = reinterpret_cast<uint64_t*>(smem + C::kOffAfull);
+    uint64_t* aslot = reinterpret_cast<uint64_t*>(smem + C::kOffAslot);
     uint64_t* yempty = reinterpret_cast<uint64_t*>(smem + C::kOffYempty);
     double2* tpart = reinterpret_cast<double2*>(smem + C::kOffTpart);
     uint64_t* pready = reinterpret_cast<uint64_t*>(smem + C::kOffPready);
@@ -308,21 +354,32 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
     const int nblk = (int)a.nblk;
     const bool rev = a.rev != 0;
     auto phys = [&](int64_t i) -> int64_t { return rev ? n - 1 - i : i; };
-    const int role = blockIdx.x < C::kCluster ? (int)blockIdx.x : -1;   // 0 chain, 1..3 lieutenants
+    const int role = blockIdx.x < C::kCluster ? (int)blockIdx.x : -1;   // 0 chain, 1.. lieutenants
     const bool chain = role == 0;
 
     if (tid == 0) {
-        for (int s = 0; s < C::kStages; s++) {
+        for (int s = 0; s < C::kNS; s++) {
             mbar_init(full + s, 1);
-            mbar_init(empty + s, chain ? 2 + C::kTeam : 1);   // chain CTA: the y team's 2 warps + each team warp
+            mbar_init(empty + s, chain ? 2 : 1);   // chain CTA: the y team's 2 warps
         }
-        for (int j = 0; j < C::kRing; j++) mbar_init(xbar + j, 1);
+        for (int j = 0; j < 2; j++) {
+            mbar_init(aready + j, 1);
+            mbar_init(aempty + j, 2);
+        }
+        for (int j = 0; j < C::kAStages; j++) {
+            mbar_init(afull + j, 1);
+            mbar_init(aslot + j, 1);
+        }
+        for (int s = 0; s < C::kSStages; s++) mbar_init(rfull + s, 1);
+        for (int s = 0; s < C::kGStages; s++) {
+            mbar_init(gfull + s, 1);
+            mbar_init(gempty + s, C::kTeam);   // the warps of the team of block k
+        }
+        for (int j = 0; j < C::kRingLt; j++) mbar_init(xbar + j, 1);
         for (int j = 0; j < C::kPbuf; j++) mbar_init(pbar + j, 1);
-        for (int j = 0; j < C::kYbuf; j++) {
-            mbar_init(yfull + j, 2);
-            mbar_init(yempty + j, C::kTeam);
-        }
-        for (int j = 0; j < 2; j++) mbar_init(pready + j, C::kTeam);
+        for (int j = 0; j < C::kRing; j++) mbar_init(xfull + j, 1);
+        for (int j = 0; j < C::kYbuf; j++) mbar_init(yempty + j, C::kTeam);
+        for (int j = 0; j < 4; j++) mbar_init(pready + j, C::kTeam + 2);   // a team's warps + the y team's 2
         *sDone = 0;
         *sF = 0;
         *sLock = 0;
@@ -332,159 +389,249 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
     cluster_sync();   // barriers and counters of every CTA initialised before any DSMEM access
 
     if (role >= 0) {
-        const int nst = chain ? C::kStages : C::kLtStages;
-        const size_t stsz = chain ? C::kChainStage : C::kLtStage;
+        const int nst = chain ? C::kSStages : C::kLtStages;
+        const size_t stsz = chain ? C::kSStage : C::kLtStage;
+        unsigned char* const sbase = smem + (chain ? C::kOffSR : 0);
         const int wprod = chain ? C::kWProducerChain : C::kCompute / 32;
         if (warp == wprod) {
-            // ------------------------------------------------ producer: TMA staging
+            // ------------------------------------------------ producer: TMA staging; lane 0 the
+            // S ring (lieutenants: list B), lane 1 the chain's G ring (independent of the helpers)
             if (lane == 0) {
+                // lieutenants: the list bounds of block k+1 are loaded while block k's slot drains
+                int64_t nb0 = 0, nb1 = 0;
+                if (!chain && nblk > 0) {
+                    nb0 = __ldg(a.nbpB + (role - 1));
+                    nb1 = __ldg(a.nbpB + role);
+                }
                 for (int k = 0; k < nblk; k++) {
                     const int s = k % nst;
-                    if (k >= nst) mbar_wait(empty + s, (uint32_t)((k / nst - 1) & 1));
-                    unsigned char* st = smem + stsz * s;
-                    if (chain) {
-                        while (ld_acquire(a.fflag + k) != epoch) __nanosleep(kProducerSleep);
-                        if (trace) trace[(int64_t)k * kTrace + 5] = gtime();
-                        fence_proxy_async();   // r_k (generic-proxy stores of a helper) -> TMA reads
-                        const uint32_t nb = stage_near(nullptr, nullptr, nullptr, a.nbpA, a.ncolA, a.nvalA,
-                                                       a.nlocA, k, C::kNloc, full + s, false);
-                        mbar_expect_tx(full + s, (uint32_t)(C::kPK * 16 + 2 * B * B * 16 + B * 16) + nb);
-                        bulk_g2s(st + C::kOffInv, a.dinv + (int64_t)k * C::kPK, C::kPK * 16, full + s);
-                        bulk_g2s(st + C::kOffG, a.G + (int64_t)k * 2 * B * B, 2 * B * B * 16, full + s);
-                        stage_near(st + C::kOffAcol, st + C::kOffAval, st + C::kOffAloc, a.nbpA, a.ncolA, a.nvalA,
-                                   a.nlocA, k, C::kNloc, full + s, true);
-                        bulk_g2s(st + C::kOffRfar, a.rfar + (int64_t)k * B, B * 16, full + s);
-                    } else {
-                        const uint32_t nb = stage_near(nullptr, nullptr, nullptr, a.nbpB, a.ncolB, a.nvalB,
-                                                       a.nlocB, k, C::kNloc, full + s, false);
-                        mbar_expect_tx(full + s, nb);
-                        stage_near(st + C::kOffBcol, st + C::kOffBval, st + C::kOffBloc, a.nbpB, a.ncolB, a.nvalB,
-                                   a.nlocB, k, C::kNloc, full + s, true);
+                    const int64_t b0 = nb0, b1 = nb1;
+                    if (!chain && k + 1 < nblk) {
+                        const int gn = (k + 1) * C::kLt + (role - 1);
+                        nb0 = __ldg(a.nbpB + gn);
+                        nb1 = __ldg(a.nbpB + gn + 1);
                     }
+                    if (k >= nst) mbar_wait(empty + s, (uint32_t)((k / nst - 1) & 1));
+                    unsigned char* st = sbase + stsz * s;
+                    if (chain) {
+                        // D_k^{-1} as soon as the slot is free; r_k (on its own barrier) once the
+                        // helpers have published it
+                        mbar_expect_tx(full + s, (uint32_t)(C::kPK * 16));
+                        bulk_g2s(st + C::kOffInv, a.dinv + (int64_t)k * C::kPK, C::kPK * 16, full + s);
+                        if (trace) STAMP(k, 9);
+                        while (ld_acquire(a.fflag + k) != epoch) __nanosleep(kProducerSleep);
+                        if (trace) STAMP(k, 5);
+                        fence_proxy_async();   // r_k (generic-proxy stores of a helper) -> TMA reads
+                        mbar_expect_tx(rfull + s, (uint32_t)(B * 16));
+                        bulk_g2s(st + C::kOffRfar, a.rfar + (int64_t)k * B, B * 16, rfull + s);
+                    } else {
+                        const int g = k * C::kLt + (role - 1);   // this lieutenant's rows of block k
+                        stage_near(st + C::kOffBcol, st + C::kOffBval, st + C::kOffBloc, b0, b1, a.ncolB, a.nvalB,
+                                   a.nlocB, g, C::kNloc, full + s);
+                    }
+                }
+            }
+        } else if (chain && warp == C::kWGProducer) {
+            // ------------------------------------------------ G producer: the teams' G ring and the
+            // A warp's list A ring (both static)
+            if (lane == 0) {
+                int64_t nb0 = 0, nb1 = 0;
+                if (nblk > 0) {
+                    nb0 = __ldg(a.nbpA);
+                    nb1 = __ldg(a.nbpA + 1);
+                }
+                for (int k = 0; k < nblk; k++) {
+                    const int s = k % C::kGStages;
+                    if (k >= C::kGStages) mbar_wait(gempty + s, (uint32_t)((k / C::kGStages - 1) & 1));
+                    mbar_expect_tx(gfull + s, (uint32_t)C::kGStage);
+                    bulk_g2s(smem + C::kGStage * s, a.G + (int64_t)k * kDense * B * B, (uint32_t)C::kGStage,
+                             gfull + s);
+                    const int sa = k % C::kAStages;
+                    const int64_t b0 = nb0, b1 = nb1;
+                    if (k + 1 < nblk) {
+                        nb0 = __ldg(a.nbpA + k + 1);
+                        nb1 = __ldg(a.nbpA + k + 2);
+                    }
+                    if (k >= C::kAStages) mbar_wait(aslot + sa, (uint32_t)((k / C::kAStages - 1) & 1));
+                    unsigned char* st = smem + C::kOffAR + C::kAStage * sa;
+                    stage_near(st + C::kOffAcol, st + C::kOffAval, st + C::kOffAloc, b0, b1, a.ncolA, a.nvalA, a.nlocA,
+                               k, C::kNloc, afull + sa);
                 }
             }
         } else if (chain && warp == C::kWPublisher) {
             // ------------------------------------------------ publisher: x blocks from the ring to
-            // global memory (and through the iLUTP column permutation to the output), to the
-            // lieutenants' rings (st.async, completing their mbarrier transactions), then the
+            // global memory (and through the iLUTP column permutation to the output), then the
             // gpu-scope frontier word
-            uint32_t peer_ring[C::kLt], peer_xbar[C::kLt];
-#pragma unroll
-            for (int l = 0; l < C::kLt; l++) {
-                peer_ring[l] = mapa(smem_u32(ring), (uint32_t)(l + 1));
-                peer_xbar[l] = mapa(smem_u32(xbar), (uint32_t)(l + 1));
+            // Blocks already complete are copied in one batch (up to 8) before the frontier
+            // word is released; the output permutation of the next block is prefetched.
+            auto perm_of = [&](int j) -> int64_t {
+                const int64_t i = (int64_t)j * B + lane;
+                return (a.operm && j < nblk && i < n) ? __ldg(a.operm + phys(i)) : 0;
+            };
+            int64_t op = perm_of(0);
+            for (int j = 0; j < nblk;) {
+                mbar_wait(xfull + j % C::kRing, (uint32_t)((j / C::kRing) & 1));
+                const int j_end = min(nblk, j + 8);
+                do {
+                    const int64_t i = (int64_t)j * B + lane;
+                    const double2 v = ring[i & kRingMask];
+                    const int64_t opj = op;
+                    op = perm_of(j + 1);
+                    if (i < n) {
+                        x[phys(i)] = v;
+                        if (a.operm) out[opj] = v;
+                    }
+                    j++;
+                } while (j < j_end && mbar_test(xfull + j % C::kRing, (uint32_t)((j / C::kRing) & 1)));
+                __syncwarp();
+                if (lane == 0) {
+                    st_release64(a.xfront, ((unsigned long long)epoch << 32) | (unsigned)j);
+                    st_rel_cta(sPub, j);
+                }
             }
-            int published = 0;
-            while (published < nblk) {
-                const int d = ld_acq_cta(sDone);
-                if (d > published) {
-                    for (int j = published; j < d; j++) {
-                        const int64_t i = (int64_t)j * B + lane;
-                        const double2 v = ring[i & kRingMask];
-#pragma unroll
-                        for (int l = 0; l < C::kLt; l++)
-                            st_async2(peer_ring[l] + (uint32_t)((i & kRingMask) * 16), v,
-                                      peer_xbar[l] + (uint32_t)((j % C::kRing) * 8));
-                        if (i < n) {
-                            const int64_t pi = phys(i);
-                            x[pi] = v;
-                            if (a.operm) out[a.operm[pi]] = v;
-                        }
+        } else if (chain && warp == C::kWA) {
+            // ------------------------------------------------ A warp: a_k = T_{k,k-kDA} x_{k-kDA}
+            // (list A, one thread per row), into abuf for the y warps
+            const int r = lane;
+            for (int k = 0; k < nblk; k++) {
+                const int s = k % C::kAStages, ab = k & 1;
+                unsigned char* st = smem + C::kOffAR + C::kAStage * s;
+                mbar_wait(afull + s, (uint32_t)((k / C::kAStages) & 1));
+                const int32_t* loc = reinterpret_cast<const int32_t*>(st + C::kOffAloc);
+                const int32_t* col = reinterpret_cast<const int32_t*>(st + C::kOffAcol);
+                const double2* val = reinterpret_cast<const double2*>(st + C::kOffAval);
+                const int lo = loc[r], hi = loc[r + 1];
+                double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
+                if (trace && lane == 0) STAMP(k, 15);
+                if (k >= C::kDA) {
+                    mbar_wait(xfull + (k - C::kDA) % C::kRing, (uint32_t)(((k - C::kDA) / C::kRing) & 1));
+                    if (trace && lane == 0) STAMP(k, 14);
+                    int e = lo;
+                    for (; e + 1 < hi; e += 2) {
+                        const int c0 = col[e], c1 = col[e + 1];
+                        const double2 v0 = val[e], v1 = val[e + 1];
+                        acc = cfma(acc, v0, ring[c0 & kRingMask]);
+                        acc2 = cfma(acc2, v1, ring[c1 & kRingMask]);
                     }
-                    __syncwarp();
-                    if (lane == 0) {
-                        st_release64(a.xfront, ((unsigned long long)epoch << 32) | (unsigned)d);
-                        st_rel_cta(sPub, d);
-                    }
-                    published = d;
-                } else {
-                    __nanosleep(kPublisherSleep);
+                    if (e < hi) acc = cfma(acc, val[e], ring[col[e] & kRingMask]);
+                }
+                if (k >= 2) mbar_wait(aempty + ab, (uint32_t)((k / 2 - 1) & 1));   // y read block k-2's
+                abuf[ab * B + r] = cadd(acc, acc2);
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(aready + ab);
+                    mbar_arrive(aslot + s);
+                    if (trace) STAMP(k, 11);
                 }
             }
         } else if (chain && warp >= C::kTeamW0) {
-            // ------------------------------------------------ chain team (4 warps):
-            // x_k = y_k - sum_w [ G1_k[:, slice_w] x_{k-1}[slice_w] + G2_k[:, slice_w] x_{k-2}[slice_w] ]
-            // Warp w owns 8 columns; the G2 term of block k+1 (which needs x_{k-1}) is formed
-            // in step k's tail.  One named barrier per step; every team warp then reduces the
-            // partials itself, so all of them hold x_k (lane = row) for the next step.
-            const int tw = warp - C::kTeamW0;
+            // ------------------------------------------------ chain teams A (even blocks) and B
+            // (odd blocks), 4 warps each:
+            //     x_k = y_k - sum_w [ G1_k[:, w] x_{k-1}[w] + G2_k[:, w] x_{k-2}[w] ]
+            // Warp w of a team owns 8 columns (slice w).  While the other team computes x_{k-1},
+            // the team of block k loads G1_k (registers) and forms the carry G2_k x_{k-2} from
+            // its own x_{k-2}; then only x_{k-1} (from the ring, xfull) -> G1_k x_{k-1} -> the
+            // partials (pready, which also carries y_k) -> x_k is on the chain.  Every warp
+            // reduces the partials itself; warp 0 stores x_k to the ring and releases xfull,
+            // warp 1 pushes x_k to the lieutenants.
+            const int team = (warp - C::kTeamW0) / C::kTeam;   // 0: even blocks, 1: odd
+            const int tw = (warp - C::kTeamW0) % C::kTeam;
             const int j0 = tw * C::kSlice;
-            double2 g1[C::kSlice], g2[C::kSlice];
-            auto load_g = [&](int k) {   // G1_k (stage k) and G2_{k+1} (stage k+1); release stage k
-                const int s = k % C::kStages;
-                mbar_wait(full + s, (uint32_t)((k / C::kStages) & 1));
-                const double2* G1 = reinterpret_cast<const double2*>(smem + C::kChainStage * s + C::kOffG);
+            double2* xw = reinterpret_cast<double2*>(smem + C::kOffXw) + (warp - C::kTeamW0) * B;   // my x_{k-2}
+            uint32_t peer_ring[C::kLt], peer_xbar[C::kLt];   // warp 1: the lieutenants' rings
 #pragma unroll
-                for (int u = 0; u < C::kSlice; u++) g1[u] = G1[(j0 + u) * B + lane];
-                if (k + 1 < nblk) {
-                    const int s1 = (k + 1) % C::kStages;
-                    mbar_wait(full + s1, (uint32_t)(((k + 1) / C::kStages) & 1));
-                    const double2* G2 =
-                        reinterpret_cast<const double2*>(smem + C::kChainStage * s1 + C::kOffG) + B * B;
+            for (int l = 0; l < C::kLt; l++) {
+                peer_ring[l] = mapa(smem_u32(smem + C::kOffLtRing), (uint32_t)(l + 1));
+                peer_xbar[l] = mapa(smem_u32(xbar), (uint32_t)(l + 1));
+            }
+            for (int k = team; k < nblk; k += 2) {
+                const int yb = k % C::kYbuf, pq = k & 3;
+                TPROF(k, 0);
+                // ---- off the chain (the other team is computing x_{k-1})
+                if (tw == 0 && k >= C::kRing)   // ring slot of block k held block k-8: published?
+                    while (ld_acq_cta(sPub) < k - C::kRing + 1) {
+                    }
+                double2 g1[C::kSlice];
+                double2 carry = make_double2(0.0, 0.0);   // G2_k[lane, slice] x_{k-2}[slice]
+                {
+                    const int s = k % C::kGStages;
+                    mbar_wait(gfull + s, (uint32_t)((k / C::kGStages) & 1));
+                    const double2* G = reinterpret_cast<const double2*>(smem + C::kGStage * s);
 #pragma unroll
-                    for (int u = 0; u < C::kSlice; u++) g2[u] = G2[(j0 + u) * B + lane];
+                    for (int u = 0; u < C::kSlice; u++) g1[u] = G[(j0 + u) * B + lane];
+                    if (k >= 2) {
+                        double2 c1 = make_double2(0.0, 0.0);
+#pragma unroll
+                        for (int u = 0; u < C::kSlice; u += 2) {
+                            carry = cfma(carry, G[B * B + (j0 + u) * B + lane], xw[j0 + u]);
+                            c1 = cfma(c1, G[B * B + (j0 + u + 1) * B + lane], xw[j0 + u + 1]);
+                        }
+                        carry = cadd(carry, c1);
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(gempty + s);
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(empty + s);   // this warp is done with stage k
-            };
-            double2 xk = make_double2(0.0, 0.0);      // x_{k-1}[lane]
-            double2 carry = make_double2(0.0, 0.0);   // G2_k[lane, slice] x_{k-2}[slice]
-            if (nblk > 0) load_g(0);
-            for (int k = 0; k < nblk; k++) {
-                const int yb = k % C::kYbuf;
+                TPROF(k, 1);
+                if (trace && tw == 0 && lane == 0) STAMP(k, 10);
+                // ---- the chain
                 double2 xs[C::kSlice];
+                if (k >= 1) {
+                    mbar_wait(xfull + (k - 1) % C::kRing, (uint32_t)(((k - 1) / C::kRing) & 1));   // x_{k-1}
+                    const double2* xr = ring + (((int64_t)(k - 1) * B) & kRingMask);
 #pragma unroll
-                for (int u = 0; u < C::kSlice; u++) {
-                    xs[u].x = __shfl_sync(0xffffffffu, xk.x, j0 + u);
-                    xs[u].y = __shfl_sync(0xffffffffu, xk.y, j0 + u);
+                    for (int u = 0; u < C::kSlice; u++) xs[u] = xr[j0 + u];
+                } else {
+#pragma unroll
+                    for (int u = 0; u < C::kSlice; u++) xs[u] = make_double2(0.0, 0.0);
                 }
+                TPROF(k, 2);
+                if (trace && tw == 0 && lane == 0) STAMP(k, 13);
                 double2 p0 = carry, p1 = make_double2(0.0, 0.0);
 #pragma unroll
                 for (int u = 0; u < C::kSlice; u += 2) {
                     p0 = cfma(p0, g1[u], xs[u]);
                     p1 = cfma(p1, g1[u + 1], xs[u + 1]);
                 }
-                tpart[((k & 1) * C::kTeam + tw) * B + lane] = cadd(p0, p1);
+                tpart[(pq * C::kTeam + tw) * B + lane] = cadd(p0, p1);
                 __syncwarp();
-                if (lane == 0) mbar_arrive(pready + (k & 1));   // this warp's partial is in tpart
-                // tail (off the critical path): G2_{k+1} x_{k-1} for the next step
-                double2 c0 = make_double2(0.0, 0.0), c1 = make_double2(0.0, 0.0);
-                if (k + 1 < nblk) {
+                if (lane == 0) mbar_arrive(pready + pq);   // this warp's partial is in tpart
+                TPROF(k, 3);
+                mbar_wait(pready + pq, (uint32_t)((k >> 2) & 1));   // the team's partials and y_k
+                TPROF(k, 4);
+                if (trace && tw == 0 && lane == 0) STAMP(k, 0);
+                double2 sum = tpart[(pq * C::kTeam + 0) * B + lane];
 #pragma unroll
-                    for (int u = 0; u < C::kSlice; u += 2) {
-                        c0 = cfma(c0, g2[u], xs[u]);
-                        c1 = cfma(c1, g2[u + 1], xs[u + 1]);
-                    }
-                }
-                carry = cadd(c0, c1);
-                if (k + 1 < nblk) load_g(k + 1);   // next G slices: overlaps the barrier wait
-                mbar_wait(yfull + yb, (uint32_t)((k / C::kYbuf) & 1));   // y_k
-                mbar_wait(pready + (k & 1), (uint32_t)((k >> 1) & 1));   // all team partials
-                if (trace && tw == 0 && lane == 0) trace[(int64_t)k * kTrace + 0] = gtime();
-                double2 sum = tpart[((k & 1) * C::kTeam + 0) * B + lane];
-#pragma unroll
-                for (int w = 1; w < C::kTeam; w++) sum = cadd(sum, tpart[((k & 1) * C::kTeam + w) * B + lane]);
-                xk = csub(ybuf[yb * B + lane], sum);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(yempty + yb);
+                for (int w = 1; w < C::kTeam; w++) sum = cadd(sum, tpart[(pq * C::kTeam + w) * B + lane]);
+                const double2 xk = csub(ybuf[yb * B + lane], sum);
+                TPROF(k, 5);
                 if (tw == 0) {
-                    // the ring slot of block k held block k-8: the publisher must have copied it
-                    if (k >= C::kRing)
-                        while (ld_acq_cta(sPub) < k - C::kRing + 1) {
-                        }
                     ring[((int64_t)k * B + lane) & kRingMask] = xk;
                     __syncwarp();
-                    if (lane == 0) {
-                        st_rel_cta(sDone, k + 1);   // publisher, y warps
-                        if (trace) trace[(int64_t)k * kTrace + 3] = gtime();
-                    }
+                    if (lane == 0) mbar_arrive(xfull + k % C::kRing);   // release: x_k is in the ring
+                    TPROF(k, 6);
+                    if (trace && lane == 0) STAMP(k, 3);
+                } else if (tw == 1) {
+                    // x_k to every lieutenant's ring (st.async completes 16 bytes of its xbar)
+                    const uint32_t off = (uint32_t)((((int64_t)k * B + lane) & (C::kRingLt * B - 1)) * 16);
+                    const uint32_t bar = (uint32_t)((k % C::kRingLt) * 8);
+#pragma unroll
+                    for (int l = 0; l < C::kLt; l++) st_async2(peer_ring[l] + off, xk, peer_xbar[l] + bar);
+                    if (lane == 0)   // the single arrival of the phase, expecting the block's bytes
+#pragma unroll
+                        for (int l = 0; l < C::kLt; l++) mbar_arrive_expect_tx_remote(peer_xbar[l] + bar, B * 16);
+                    if (trace && lane == 0) STAMP(k, 8);
                 }
+                xw[lane] = xk;   // my x_k: the carry of block k+2
+                __syncwarp();
+                if (lane == 0) mbar_arrive(yempty + yb);
+                TPROF(k, 7);
             }
         } else if (chain && warp >= C::kYW0) {
-            // ------------------------------------------------ y warps: y_k = D_k^{-1} (r_k - A3_k x_{k-3} - partials)
-            // 4 threads per row (r = row, q = column class): D_k^{-1}[r, j], j = q mod 4,
-            // j <= r, lives in registers; one named barrier per block (the residual vector).
-            // two y teams of 2 warps take the even / odd blocks (each has two chain steps)
+            // ------------------------------------------------ y warps:
+            // y_k = D_k^{-1} (r_k - lieutenant partials - list A product)
+            // two y teams of 2 warps take the even / odd blocks (each has two chain steps);
+            // 2 threads per row (r = row, q = column class j = q mod 2): D_k^{-1}[r, j], j <= r,
+            // lives in registers; one named barrier per block (the residual vector).
             const int yteam = (warp - C::kYW0) >> 1;           // 0: even blocks, 1: odd blocks
             const int yt = ((warp - C::kYW0) & 1) * 32 + lane;   // 0 .. 63
             constexpr int kYT = 64;
@@ -492,9 +639,10 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
             const int r = yt / kQ, q = yt % kQ;
             double2* sR = reinterpret_cast<double2*>(smem + C::kOffR) + yteam * B;   // [2][B]
             for (int k = yteam; k < nblk; k += 2) {
-                const int s = k % C::kStages, yb = k % C::kYbuf, pk = k % C::kPbuf;
-                unsigned char* st = smem + C::kChainStage * s;
-                mbar_wait(full + s, (uint32_t)((k / C::kStages) & 1));
+                const int s = k % C::kSStages, yb = k % C::kYbuf, pk = k % C::kPbuf;
+                unsigned char* st = smem + C::kOffSR + C::kSStage * s;
+                mbar_wait(full + s, (uint32_t)((k / C::kSStages) & 1));
+                if (trace && yt == 0) STAMP(k, 2);
                 const double2* sInv = reinterpret_cast<const double2*>(st + C::kOffInv);
                 double2 dv[B / kQ];
 #pragma unroll
@@ -502,25 +650,15 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     const int j = q + kQ * t;
                     dv[t] = j <= r ? sInv[j * B - (j * (j - 1)) / 2 + (r - j)] : make_double2(0.0, 0.0);
                 }
-                const double2 rf = reinterpret_cast<const double2*>(st + C::kOffRfar)[r];
-                // list A: source distance 3 (x_{k-3}, in the ring once the team has done it)
-                if (k >= 3)
-                    while (ld_acq_cta(sDone) < k - 2) {
-                    }
-                if (trace && yt == 0) trace[(int64_t)k * kTrace + 2] = gtime();
-                double2 acc = near_part<B, kQ>(reinterpret_cast<const int32_t*>(st + C::kOffAloc),
-                                               reinterpret_cast<const int32_t*>(st + C::kOffAcol),
-                                               reinterpret_cast<const double2*>(st + C::kOffAval), ring, r, q);
-#pragma unroll
-                for (int o = 1; o < kQ; o <<= 1) {
-                    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-                    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
-                }
                 if (yt == 0) mbar_expect_tx(pbar + pk, (uint32_t)(B * 16));
+                mbar_wait(rfull + s, (uint32_t)((k / C::kSStages) & 1));   // r_k
+                const double2 rf = reinterpret_cast<const double2*>(st + C::kOffRfar)[r];
                 mbar_wait(pbar + pk, (uint32_t)((k / C::kPbuf) & 1));   // lieutenants' partials
-                if (trace && yt == 0) trace[(int64_t)k * kTrace + 6] = gtime();
-                if (q == 0) sR[r] = csub(csub(rf, acc), pbuf[pk * B + r]);
+                if (trace && yt == 0) STAMP(k, 6);
+                mbar_wait(aready + (k & 1), (uint32_t)((k >> 1) & 1));   // list A product
+                if (q == 0) sR[r] = csub(csub(rf, pbuf[pk * B + r]), abuf[(k & 1) * B + r]);
                 bar_named(2 + yteam * 2, kYT);   // the team's residual vector is complete
+                if (lane == 0) mbar_arrive(aempty + (k & 1));
                 double2 y0 = make_double2(0.0, 0.0), y1 = make_double2(0.0, 0.0);
 #pragma unroll
                 for (int t = 0; t < B / kQ; t += 2) {
@@ -539,38 +677,46 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                 }
                 __syncwarp();
                 if (lane == 0) {
-                    mbar_arrive(yfull + yb);   // one arrival per y warp of the team (its 16 rows)
+                    mbar_arrive(pready + (k & 3));   // y_k: one arrival per y warp (its 16 rows)
                     mbar_arrive(empty + s);
-                    if (trace && yt == 0) trace[(int64_t)k * kTrace + 1] = gtime();
+                    if (trace && yt == 0) STAMP(k, 1);
                 }
                 bar_named(2 + yteam * 2, kYT);   // sR is reused by the team's next block
             }
         } else if (!chain) {
             // ------------------------------------------------ lieutenants: list B partial sums
-            const int l = role - 1;   // rows l, l+3, l+6, ...
+            // (source distance kDA+1 .. Q_k-1) of the rows l, l+kLt, ...; two teams of 4
+            // warps take the even / odd blocks.  The early part (distance >= kDA+2) is
+            // summed before x_{k-kDA-1} lands, the late part after.  x blocks land by
+            // st.async from the chain team, which also makes each xbar phase's one arrival.
+            const int l = role - 1;
             const uint32_t peer_pbuf = mapa(smem_u32(pbuf), 0u);
             const uint32_t peer_pbar = mapa(smem_u32(pbar), 0u);
+            const double2* ltring = reinterpret_cast<const double2*>(smem + C::kOffLtRing);
+            const int lteam = tid / C::kLtTeamT, tt = tid % C::kLtTeamT;
             int xseen = 0;   // x blocks < xseen have landed in the ring
-            const int r = l + C::kLt * (tid / C::kTPRl), q = tid % C::kTPRl;
+            const int r = l + C::kLt * (tt / C::kTPRl), q = tt % C::kTPRl;
             const bool rowok = r < B;
+            auto land = [&](int upto) {   // wait for the xbar phases of blocks xseen .. upto, in order
+                for (; xseen <= upto; xseen++)
+                    mbar_wait(xbar + xseen % C::kRingLt, (uint32_t)((xseen / C::kRingLt) & 1));
+            };
             if (warp < C::kCompute / 32) {
-                for (int k = 0; k < nblk; k++) {
+                for (int k = lteam; k < nblk; k += 2) {
                     const int s = k % nst;
                     unsigned char* st = smem + stsz * s;
                     mbar_wait(full + s, (uint32_t)((k / nst) & 1));
-                    // list B of block k reads x of blocks <= k - 4: consume their arrivals in
-                    // order (each xbar phase exactly once)
-                    for (; xseen <= k - 4; xseen++) {
-                        const int j = xseen % C::kRing;
-                        if (tid == 0) mbar_expect_tx(xbar + j, (uint32_t)(B * 16));
-                        mbar_wait(xbar + j, (uint32_t)((xseen / C::kRing) & 1));
-                    }
-                    if (trace && tid == 0 && l == 0) trace[(int64_t)k * kTrace + 7] = gtime();
+                    const bool tr0 = trace && tt == 0 && l == 0;
+                    if (tr0) STAMP(k, 12);
+                    const int32_t* loc = reinterpret_cast<const int32_t*>(st + C::kOffBloc);
+                    const int32_t* col = reinterpret_cast<const int32_t*>(st + C::kOffBcol);
+                    const double2* val = reinterpret_cast<const double2*>(st + C::kOffBval);
                     double2 acc = make_double2(0.0, 0.0);
-                    if (rowok)
-                        acc = near_part<B, C::kTPRl>(reinterpret_cast<const int32_t*>(st + C::kOffBloc),
-                                                     reinterpret_cast<const int32_t*>(st + C::kOffBcol),
-                                                     reinterpret_cast<const double2*>(st + C::kOffBval), ring, r, q);
+                    land(k - C::kDA - 2);
+                    if (rowok) acc = near_range<B, C::kTPRl, C::kRingLt>(col, val, ltring, loc[r], loc[C::kLate + r], q, acc);
+                    land(k - C::kDA - 1);
+                    if (tr0) STAMP(k, 7);
+                    if (rowok) acc = near_range<B, C::kTPRl, C::kRingLt>(col, val, ltring, loc[C::kLate + r], loc[r + 1], q, acc);
 #pragma unroll
                     for (int o = 1; o < C::kTPRl; o <<= 1) {
                         acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
@@ -580,14 +726,16 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                         const int pk = k % C::kPbuf;
                         st_async2(peer_pbuf + (uint32_t)((pk * B + r) * 16), acc, peer_pbar + (uint32_t)(pk * 8));
                     }
-                    bar_named(2, C::kCompute);
-                    if (tid == 0) mbar_arrive(empty + s);
+                    bar_named(2 + lteam, C::kLtTeamT);
+                    if (tt == 0) {
+                        mbar_arrive(empty + s);
+
+                    }
                 }
-                for (; xseen < nblk; xseen++) {   // drain the remaining arrivals before leaving
-                    const int j = xseen % C::kRing;
-                    if (tid == 0) mbar_expect_tx(xbar + j, (uint32_t)(B * 16));
-                    mbar_wait(xbar + j, (uint32_t)((xseen / C::kRing) & 1));
-                }
+                // before leaving, every x push to this CTA has landed: the last phase of each
+                // xbar slot (earlier phases of a slot completed before it)
+                if (xseen < nblk - C::kRingLt) xseen = nblk - C::kRingLt;
+                land(nblk - 1);
             }
         }
         // no CTA of the cluster leaves while a peer may still access its shared memory
@@ -663,7 +811,7 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
         bar_named(1, C::kCompute);
         if (tid == 0) {
             st_release(a.fflag + k, epoch);
-            if (trace) trace[(int64_t)k * kTrace + 4] = gtime();
+            if (trace) STAMP(k, 4);
         }
     }
 }

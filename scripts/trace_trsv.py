@@ -36,21 +36,36 @@ def main():
         prev = tr[:-1, 5]
         done_prev = tr[:-1, 3]
         med = lambda v: float(np.median(v))
+        step = tr[1:, 3] - tr[:-1, 3]
+        ex = np.maximum(0, step - med(step))
         d = {
             "blocks": int(tr.shape[0]),
             "total_us": float(tr[:, 3].max() / 1e3),
-            "step_ns": med(tr[1:, 3] - tr[:-1, 3]),
-            "team_barrier_minus_prev_done_ns": med(rel[:, 0] - done_prev),
-            "team_reduce_publish_ns": med(tr[:, 3] - tr[:, 0]),
-            "y_done_minus_prev_done_ns": med(rel[:, 1] - done_prev),
-            "y_late_frac": float(np.mean(rel[:, 1] > rel[:, 0])),
-            "y_start_minus_prev_done_ns": med(rel[:, 2] - done_prev),
-            "y_near_and_pbar_ns": med(tr[:, 6] - tr[:, 2]),
-            "y_rest_ns": med(tr[:, 1] - tr[:, 6]),
-            "y_start_minus_prev_y_done_ns": med(tr[1:, 2] - tr[:-1, 1]),
-            "lieutenant_start_minus_prev_done_ns": med(rel[:, 7] - done_prev),
-            "helper_publish_minus_prev_done_ns": med(rel[:, 4] - done_prev),
-            "chain_waited_on_helpers_frac": float(np.mean(rel[:, 5] > done_prev)),
+            "step_ns": med(step),
+            "step_pct_ns": [float(v) for v in np.percentile(step, [10, 50, 90, 99])],
+            "excess_us": float(ex.sum() / 1e3),
+            "excess_helper_late_us": float(np.sum(np.where(rel[:, 5] > done_prev - 2000, ex, 0)) / 1e3),
+            # chain team (relative to x_{k-1} stored)
+            "team_tail_done_ns": med(rel[:, 10] - done_prev),
+            "team_ready_ns": med(rel[:, 0] - done_prev),
+            "team_reduce_store_ns": med(tr[:, 3] - tr[:, 0]),
+            "team_push_minus_store_ns": med(tr[:, 8] - tr[:, 3]),
+            # y warps
+            "y_stage_ready_ns": med(rel[:, 2] - done_prev),
+            "y_pbar_ns": med(rel[:, 6] - done_prev),
+            "team_g1_loaded_ns": med(rel[:, 13] - done_prev),
+            "a_stage_ready_ns": med(rel[:, 15] - done_prev),
+            "a_saw_xkm3_ns": med(rel[:, 14] - done_prev),
+            "a_done_ns": med(rel[:, 11] - done_prev),
+            "y_done_ns": med(rel[:, 1] - done_prev),
+            # lieutenant 0 (relative to x_{k-1} stored)
+            "lt_stage_ready_ns": med(rel[:, 12] - done_prev),
+            "lt_late_landed_ns": med(rel[:, 7] - done_prev),
+            "producer_static_issued_ns": med(rel[:, 9] - done_prev),
+            "lt_late_landed_minus_push_km4_ns": med(tr[4:, 7] - tr[:-4, 8]),
+            # helpers / producer
+            "helper_publish_ns": med(rel[:, 4] - done_prev),
+            "producer_flag_pct_ns": [float(v) for v in np.percentile(rel[:, 5] - done_prev, [10, 50, 90, 99])],
             "first_blocks": tr[:3].tolist(),
         }
         out[nm] = d

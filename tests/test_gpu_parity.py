@@ -102,6 +102,37 @@ def test_spmv_and_substitutions(cuda, name):
     s.close()
 
 
+@pytest.mark.parametrize("knobs", [{"SSB_TRSV_Q": "4"}, {"SSB_TRSV_Q": "5"}, {"SSB_TRSV_Q": "9"},
+                                   {"SSB_TRSV_CAPA": "0"}])
+def test_substitution_split_variants(cuda, monkeypatch, knobs):
+    """The same substitutions with the source-distance split moved:
+    Q = 4 leaves the lieutenants' list B empty (everything beyond list A goes to the helper
+    CTAs), Q = 5 gives list B only its late part, Q = 9 a shorter window; CAPA = 0 overflows
+    every block's list A, so the helpers take every distance >= 3 (the overflow fallback)."""
+    torch = cuda
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    p = CONFIGS["small"]
+    s = pb().SteadyState(p).setup()
+    Lt, _, _, _ = lv.constrained_system(p)
+    A = R.permute(Lt, pb().ss_export_perm(s.handle))
+    F = I.ilutp(A, p.drop_tol, p.fill_factor, p.permtol)
+    x = rand_cvec(A.shape[0], 5)
+    xd = torch.from_numpy(x).cuda()
+    for _ in range(2):   # relaunch: epochs advance
+        yl = s.precond(xd, 0).cpu().numpy()
+        rl = sp.linalg.spsolve_triangular(T.lower_unit_matrix(F), x, lower=True, unit_diagonal=True)
+        assert np.abs(yl - rl).max() <= 1e-11 * np.abs(rl).max()
+        ym = s.precond(xd, 2).cpu().numpy()
+        rm = T.apply_preconditioner(F, x)
+        assert np.abs(ym - rm).max() <= 1e-10 * np.abs(rm).max()
+    if "SSB_TRSV_Q" in knobs:
+        assert max(s.setup_info["trsv_q_L"], s.setup_info["trsv_q_U"]) <= int(knobs["SSB_TRSV_Q"])
+    else:
+        assert s.setup_info["trsv_q_L"] == 3 and s.setup_info["trsv_q_U"] == 3
+    s.close()
+
+
 @pytest.mark.parametrize("name", ["tiny", "small", "ragged", "nth0", "g00", "w_given"])
 def test_steady_state_parity(cuda, name):
     p = {**CONFIGS, **EDGE}[name]
@@ -195,13 +226,14 @@ def test_sweep_points_on_gpu(cuda):
 
 
 def test_trace_abi(cuda):
-    """ss_debug_trace_trsv returns one row of 8 stamps per block of the substitution."""
+    """ss_debug_trace_trsv returns one row of SS_TRACE_STAMPS (16) stamps per block."""
     torch = cuda
     s = pb().SteadyState(CONFIGS["tiny"]).setup()
     x = torch.randn(s.n, dtype=torch.complex128, device="cuda")
     y = torch.empty_like(x)
     tr = pb().ss_debug_trace_trsv(s.handle, 0, x.data_ptr(), y.data_ptr())
-    assert tr.shape == ((s.n + 31) // 32, 8)
+    assert tr.shape == ((s.n + 31) // 32, 16)
+    assert np.all(tr[:, 3] > 0)
     ref = s.precond(x, 0)
     assert torch.equal(y, ref)      # tracing does not change the result
     s.close()
