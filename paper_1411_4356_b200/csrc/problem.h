@@ -47,14 +47,12 @@ struct HostCSR {
 // Triangular factor on the device in the block layout of trsv.cu (kernel index space:
 // L as is, U reversed i' = n-1-i so that both are lower triangular; blocks of B rows).
 // Source-distance split of the entries left of block k (d = k - source block):
-//   d = 1 .. kDense    -> dense G_d = D_k^{-1} T_{k,k-d} (the chain teams)
-//   d = kDense + 1     -> list A, staged per block in the chain CTA (the A warp)
-//   kDense+1 < d < Q_k -> list B, staged per lieutenant CTA and block
-//   d >= Q_k           -> far part (helper CTAs)
-constexpr int kDense = 2;
-constexpr int near_cap_a(int B) { return B <= 32 ? 960 : B * B; }   // list A entries per block
-constexpr int near_cap_b(int B) { return B <= 32 ? 2048 : 1536; }   // per lieutenant and block
-constexpr int kLieutenants = 3;   // list B CTAs of a chain cluster (trsv.cu)
+//   d = 1 .. kDense  -> dense G_d = D_k^{-1} T_{k,k-d} (the chain teams)
+//   kDense < d < Q_k -> list B, staged per lieutenant CTA and block
+//   d >= Q_k         -> far part (helper CTAs)
+constexpr int kDense = 3;
+constexpr int near_cap_b(int B) { return B <= 32 ? 1024 : 1024; }   // per lieutenant and block
+constexpr int kLieutenants = 7;   // list B CTAs of a chain cluster (trsv.cu; cluster = 1 + 7)
 constexpr int near_nloc(int B) { return 2 * (B + 4); }   // per list: row starts | late-part starts
 
 // one near list on the device (see setup.cpp::build_block_tri)
@@ -79,19 +77,15 @@ struct TriArgs {
     const int64_t* farptr;    // [n+1] entries of row i' with source block <= k-Q_k (k = i'/B)
     const int32_t* fcol;      //       kernel-space columns, ascending within a row
     const double2* fval;
-    const int64_t* nbpA;      // near list A: [nblk+1] (chain CTA)
-    const int32_t* ncolA;
-    const double2* nvalA;
-    const int32_t* nlocA;
     const int64_t* nbpB;      // near list B: [nblk*kLieutenants+1], list of (block k, lieutenant l) at k*kLt+l
     const int32_t* ncolB;
     const double2* nvalB;
     const int32_t* nlocB;
     const double2* dinv;      // [nblk][B(B+1)/2] inverse diagonal blocks, packed lower, column-major
     const double2* G;         // [nblk][kDense][B*B] D_k^{-1} T_{k,k-d}, d = 1 .. kDense, column-major
-    double2* rfar;            // [nblk*B] b - (far part), written by the helper CTAs
+    double2* yfar;            // [nblk*B] y_k = D_k^{-1} (b_k - far part), written by the helper CTAs
     const int64_t* operm;     // [n] output permutation out[operm[i]] = x[i] (ILUTP columns), or null
-    uint32_t* fflag;          // [nblk] "rfar of block k is ready" (value = launch epoch)
+    uint32_t* fflag;          // [nblk] "yfar of block k is ready" (value = launch epoch)
     unsigned long long* xfront;   // (epoch << 32) | number of blocks of x published
 };
 
@@ -101,10 +95,10 @@ struct DevBlockTri {
     int64_t* farptr = nullptr;
     int32_t* fcol = nullptr;
     double2* fval = nullptr;
-    NearDev nearA, nearB;
+    NearDev nearB;
     double2* dinv = nullptr;
     double2* G = nullptr;
-    double2* rfar = nullptr;
+    double2* yfar = nullptr;
     uint32_t* fflag = nullptr;
     unsigned long long* xfront = nullptr;
     int64_t* operm = nullptr;   // U of ILUTP: out[operm[p]] = x[p] (column permutation), else null
@@ -113,19 +107,17 @@ struct DevBlockTri {
     int grid = 0;
     int64_t nlev = 0;   // row-level dependency levels (diagnostic)
     TriArgs args() const {
-        return TriArgs{n,         nblk,      rev,       B,         farptr,    fcol,  fval, nearA.bp,
-                       nearA.col, nearA.val, nearA.loc, nearB.bp,  nearB.col, nearB.val, nearB.loc,
-                       dinv,      G,         rfar,      operm,     fflag,     xfront};
+        return TriArgs{n,         nblk,      rev,  B, farptr, fcol,  fval,  nearB.bp, nearB.col, nearB.val,
+                       nearB.loc, dinv,      G,    yfar,  operm,  fflag, xfront};
     }
     void release() {
         cudaFree(farptr);
         cudaFree(fcol);
         cudaFree(fval);
-        nearA.release();
         nearB.release();
         cudaFree(dinv);
         cudaFree(G);
-        cudaFree(rfar);
+        cudaFree(yfar);
         cudaFree(fflag);
         cudaFree(xfront);
         cudaFree(operm);

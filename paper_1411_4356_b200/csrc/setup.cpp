@@ -149,7 +149,7 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
     // per row: entries per source distance d = k - source block (d = 1 .. kMaxQ-1; d >= kMaxQ
     // counted together); the near window Q (near = d < Q, far = d >= Q) is the largest
     // Q <= Qmax whose per-block near lists fit the shared-memory stage (kNearCap)
-    constexpr int kMaxQ = 16;
+    constexpr int kMaxQ = 32;
     std::vector<int64_t> dcnt((size_t)n * kMaxQ, 0);   // [row][d], d = 0 means ">= kMaxQ"
     std::vector<int64_t> nin(n);                        // strict entries left of the block
     parallel_for(n, threads, [&](int64_t lo, int64_t hi) {
@@ -170,27 +170,17 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
     });
     // Split of the entries left of block k by source distance d (problem.h, trsv.cu):
     //   d = 1 .. kDense       -> dense G_d = D_k^{-1} T_{k,k-d} (the chain teams)
-    //   d = kDA = kDense+1    -> list A (the A warp of the chain CTA, one thread per row)
-    //   kDA < d < Q_k         -> list B (the lieutenant CTAs of the chain's cluster; lieutenant
+    //   kDense < d < Q_k      -> list B (the lieutenant CTAs of the chain's cluster; lieutenant
     //                            l holds the rows r = l mod kLieutenants of the block); the
-    //                            d = kDA+1 entries of each row (the last ones) form its late part
+    //                            d = kDense+1 entries of each row (the last ones) form its late part
     //   d >= Q_k              -> far (the helper CTAs)
-    // Q_k is the largest Q <= Qmax (>= kDA+1) whose per-lieutenant lists fit their stages; a
-    // block whose list A overflows its stage takes Q_k = kDA (d >= kDA to the helpers).
-    // A row's entries in ascending column: far | list B (late part last) | list A | G_kDense ..
-    // G_1 | block.
-    constexpr int kDA = kDense + 1, kD1 = kDA + 1;
+    // Q_k is the largest Q <= Qmax (>= kDense+1) whose per-lieutenant lists fit their stages.
+    // A row's entries in ascending column: far | list B (late part last) | G_kDense .. G_1 | block.
+    constexpr int kD1 = kDense + 1;
     const int qmax = std::max(kD1, std::min(kMaxQ, q_max));
-    const int capa = std::min(near_cap_a(B), env_int("SSB_TRSV_CAPA", near_cap_a(B)));   // (tests lower it)
     std::vector<int> qk(nblk, qmax);
     parallel_for(nblk, threads, [&](int64_t lo, int64_t hi) {
         for (int64_t k = lo; k < hi; k++) {
-            int64_t ca = 0;
-            for (int64_t ip = k * B; ip < std::min(n, (k + 1) * B); ip++) ca += dcnt[(size_t)ip * kMaxQ + kDA];
-            if (ca + 3 > capa) {
-                qk[k] = kDA;
-                continue;
-            }
             int q = qmax;
             for (; q > kD1; q--) {
                 int64_t cb[kLieutenants] = {};
@@ -206,29 +196,28 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
     int qmin = qmax;
     for (int64_t k = 0; k < nblk; k++) qmin = std::min(qmin, qk[k]);
     T.Q = qmin;
-    // per row: far / list B (its late part) / list A / dense G_d entries
-    std::vector<int64_t> cnt(n), acnt(n), bcnt(n), blate(n), gcnt((size_t)n * kDense);
+    // per row: far / list B (its late part) / dense G_d entries
+    std::vector<int64_t> cnt(n), bcnt(n), blate(n), gcnt((size_t)n * kDense);
     for (int64_t ip = 0; ip < n; ip++) {
         const int q = qk[ip / B];
         int64_t nbb = 0, ng = 0;
         for (int d = kD1; d < q; d++) nbb += dcnt[(size_t)ip * kMaxQ + d];
         for (int d = 1; d <= kDense; d++) ng += (gcnt[(size_t)ip * kDense + d - 1] = dcnt[(size_t)ip * kMaxQ + d]);
-        acnt[ip] = q > kDA ? dcnt[(size_t)ip * kMaxQ + kDA] : 0;
         bcnt[ip] = nbb;
         blate[ip] = q > kD1 ? dcnt[(size_t)ip * kMaxQ + kD1] : 0;
-        cnt[ip] = nin[ip] - ng - acnt[ip] - nbb;
+        cnt[ip] = nin[ip] - ng - nbb;
     }
     std::vector<int64_t>().swap(dcnt);
     std::vector<int64_t> farptr(n + 1, 0);
     for (int64_t i = 0; i < n; i++) farptr[i + 1] = farptr[i] + cnt[i];
-    // near lists: per (block, group) a padded start, per row a local pointer and the local
-    // start of its late part (list A: one group, no late part; list B: a group per lieutenant)
+    // list B: per (block, lieutenant) a padded start, per row a local pointer and the local
+    // start of its late part
     struct NearHost {
         std::vector<int64_t> bp, row;   // list starts [nblk*G+1], global row starts [n]
         std::vector<int32_t> loc;       // [nblk*G][2(B+4)]
     };
     const int NL = near_nloc(B);
-    auto layout = [&](const std::vector<int64_t>& c, const std::vector<int64_t>* late, int G, NearHost& H) {
+    auto layout = [&](const std::vector<int64_t>& c, const std::vector<int64_t>& late, int G, NearHost& H) {
         H.bp.assign(nblk * G + 1, 0);
         H.row.assign(n, 0);
         H.loc.assign((size_t)nblk * G * NL, 0);
@@ -244,7 +233,7 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
                     if (ip < n && r % G == g) {
                         H.row[ip] = H.bp[idx] + off;
                         off += c[ip];
-                        loc[B + 4 + r] = (int32_t)(off - (late ? (*late)[ip] : 0));
+                        loc[B + 4 + r] = (int32_t)(off - late[ip]);
                     }
                 }
                 for (int r = B; r < B + 4; r++) loc[r] = loc[B + 4 + r] = (int32_t)off;
@@ -252,10 +241,9 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
             }
     };
     constexpr int G = kLieutenants;
-    NearHost HA, HB;
-    layout(acnt, nullptr, 1, HA);
-    layout(bcnt, &blate, G, HB);
-    const int64_t nf = farptr[n], nA = HA.bp[nblk], nB = HB.bp[nblk * G];
+    NearHost HB;
+    layout(bcnt, blate, G, HB);
+    const int64_t nf = farptr[n], nB = HB.bp[nblk * G];
     T.nnz_far = nf;
     T.nnz_near = 0;
     for (int64_t i = 0; i < n; i++) T.nnz_near += nin[i] - cnt[i];
@@ -273,11 +261,10 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
     SSB_CUDA(cudaMalloc(&T.farptr, (n + 1) * sizeof(int64_t)));
     SSB_CUDA(cudaMalloc(&T.fcol, std::max<int64_t>(1, nf) * sizeof(int32_t)));
     SSB_CUDA(cudaMalloc(&T.fval, std::max<int64_t>(1, nf) * sizeof(double2)));
-    upload_near(HA, nA, T.nearA);
     upload_near(HB, nB, T.nearB);
     SSB_CUDA(cudaMalloc(&T.dinv, std::max<int64_t>(1, nblk * PK) * sizeof(double2)));
     SSB_CUDA(cudaMalloc(&T.G, std::max<int64_t>(1, nblk * kDense * B * B) * sizeof(double2)));
-    SSB_CUDA(cudaMalloc(&T.rfar, std::max<int64_t>(1, nblk * B) * sizeof(double2)));
+    SSB_CUDA(cudaMalloc(&T.yfar, std::max<int64_t>(1, nblk * B) * sizeof(double2)));
     SSB_CUDA(cudaMalloc(&T.fflag, std::max<int64_t>(1, nblk) * sizeof(uint32_t)));
     SSB_CUDA(cudaMalloc(&T.xfront, sizeof(unsigned long long)));
     SSB_CUDA(cudaMemsetAsync(T.fflag, 0, std::max<int64_t>(1, nblk) * sizeof(uint32_t), s));
@@ -288,29 +275,25 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
     // entries, in block chunks of ~2^26 (bounded host staging); the rows of a chunk of
     // blocks map to contiguous ranges of the far CSR and of list B
     const int64_t kChunk = (int64_t)1 << 26;
-    std::vector<int32_t> fc, ac, bc;
-    std::vector<double2> fv, av, bv;
+    std::vector<int32_t> fc, bc;
+    std::vector<double2> fv, bv;
     auto frow = [&](int64_t k) { return farptr[std::min(n, k * B)]; };
     for (int64_t k0 = 0; k0 < nblk;) {
         int64_t k1 = k0 + 1;
-        while (k1 < nblk && (frow(k1 + 1) - frow(k0)) + (HA.bp[k1 + 1] - HA.bp[k0]) +
-                                    (HB.bp[(k1 + 1) * G] - HB.bp[k0 * G]) <= kChunk)
+        while (k1 < nblk && (frow(k1 + 1) - frow(k0)) + (HB.bp[(k1 + 1) * G] - HB.bp[k0 * G]) <= kChunk)
             k1++;
         const int64_t r0 = k0 * B, r1 = std::min(n, k1 * B);
         const int64_t fb = farptr[r0], flen = farptr[r1] - fb;
-        const int64_t ab = HA.bp[k0], alen = HA.bp[k1] - ab;
         const int64_t bb = HB.bp[k0 * G], blen = HB.bp[k1 * G] - bb;
         fc.resize(flen);
         fv.resize(flen);
-        ac.assign(alen, 0);
-        av.assign(alen, make_double2(0.0, 0.0));
         bc.assign(blen, 0);
         bv.assign(blen, make_double2(0.0, 0.0));
         parallel_for(r1 - r0, threads, [&](int64_t lo, int64_t hi) {
             for (int64_t ip = r0 + lo; ip < r0 + hi; ip++) {
                 int64_t q0, q1;
                 row_range(ip, q0, q1);
-                // row layout (ascending column = descending distance): far | list B | list A | dense | block
+                // row layout (ascending column = descending distance): far | list B | dense | block
                 int64_t t = 0;
                 for (int64_t u = 0; u < cnt[ip]; u++, t++) {
                     const int64_t q = entry(q0, q1, t);
@@ -322,20 +305,11 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
                     bc[HB.row[ip] - bb + u] = (int32_t)kcol(q);
                     bv[HB.row[ip] - bb + u] = F.val[q];
                 }
-                for (int64_t u = 0; u < acnt[ip]; u++, t++) {
-                    const int64_t q = entry(q0, q1, t);
-                    ac[HA.row[ip] - ab + u] = (int32_t)kcol(q);
-                    av[HA.row[ip] - ab + u] = F.val[q];
-                }
             }
         });
         if (flen) {
             SSB_CUDA(cudaMemcpy(T.fcol + fb, fc.data(), flen * sizeof(int32_t), cudaMemcpyHostToDevice));
             SSB_CUDA(cudaMemcpy(T.fval + fb, fv.data(), flen * sizeof(double2), cudaMemcpyHostToDevice));
-        }
-        if (alen > 0) {
-            SSB_CUDA(cudaMemcpy(T.nearA.col + ab, ac.data(), alen * sizeof(int32_t), cudaMemcpyHostToDevice));
-            SSB_CUDA(cudaMemcpy(T.nearA.val + ab, av.data(), alen * sizeof(double2), cudaMemcpyHostToDevice));
         }
         if (blen > 0) {
             SSB_CUDA(cudaMemcpy(T.nearB.col + bb, bc.data(), blen * sizeof(int32_t), cudaMemcpyHostToDevice));
@@ -457,7 +431,7 @@ void setup_problem(Problem& P, double drop_tol, double fill_factor, double permt
     SSB_CUDA(cudaMemcpyAsync(P.d_perm, P.perm.data(), P.n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
     if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
     const int B = env_int("SSB_TRSV_B", 32);
-    const int QMAX = env_int("SSB_TRSV_Q", 16);
+    const int QMAX = env_int("SSB_TRSV_Q", 32);
     int64_t levL = 0, levU = 0;
     std::thread lev([&] {
         levL = count_levels(P.hL, false);

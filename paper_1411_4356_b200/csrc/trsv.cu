@@ -164,68 +164,57 @@ struct Cfg {
     static constexpr int kLt = kLieutenants;
     static constexpr int kCluster = 1 + kLt;          // chain + lieutenants
     static constexpr int kCompute = 256;              // compute threads (8 warps)
-    static constexpr int kNT = 512;                   // chain CTA: 16 warps (roles below)
+    static constexpr int kNT = 544;                   // chain CTA: 17 warps (roles below)
     // chain CTA warp roles (warp w runs on SMSP w mod 4): producer 0, publisher 1, G producer
-    // 2, A warp 3 (list A), y warps 4 .. 7 (two y teams of two), chain teams A = warps 8 .. 11
-    // (even blocks) and B = 12 .. 15 (odd blocks), one warp of each team per SMSP
-    static constexpr int kTeam = 4, kTeamW0 = 8;
-    static constexpr int kYW0 = 4;
-    static constexpr int kWProducerChain = 0, kWPublisher = 1, kWGProducer = 2, kWA = 3;
-    static constexpr int kDA = kDense + 1;            // list A source distance
+    // 2, chain teams 0, 1, 2 = warps 5 .. 8, 9 .. 12, 13 .. 16 (blocks k = team mod 3), one
+    // warp of each team per SMSP (warps 3, 4 idle)
+    static constexpr int kTeam = 4, kTeams = 3, kTeamW0 = 5;
+    static constexpr int kWProducerChain = 0, kWPublisher = 1, kWGProducer = 2;
     static constexpr int kSlice = B / kTeam;          // columns of G per team warp
     static constexpr int kFarWarps = kCompute / 32;   // helper warps streaming the far part
     static constexpr int kRPW = B / kFarWarps;        // far rows per helper warp
     static constexpr int kGrp = kRPW < 4 ? kRPW : 4;
-    static constexpr int kGStages = 3;                // G1 | G2 ring (chain teams, a block ahead)
-    static constexpr int kSStages = 4;                // D^{-1} / r ring (y warps)
-    static constexpr int kAStages = 3;                // list A ring (A warp)
-    static constexpr int kCapA = near_cap_a(B);
-    static constexpr int kRing = 8;                   // chain CTA: x of the last 8 blocks
-    static constexpr int kRingLt = 16;                // lieutenants: x of the last 16 blocks (Q <= 16)
+    static constexpr int kGStages = 3;                // G1 | G2 | G3 ring (chain teams, a block ahead)
+    static constexpr int kSStages = 16;               // y_k ring (the helpers' D_k^{-1} (b_k - far))
+    static constexpr int kRing = 16;                  // chain CTA: x of the last 16 blocks
+    static constexpr int kRingLt = 32;                // lieutenants: x of the last 32 blocks (Q <= 32)
     static constexpr int kPbuf = 4;                   // lieutenant partial-sum slots
-    static constexpr int kYbuf = 2;                   // y slots
     static constexpr int kPK = B * (B + 1) / 2;
     static constexpr int kCapB = near_cap_b(B);
     static constexpr int kNloc = near_nloc(B);        // per list: row starts | late-part starts
     static constexpr int kLate = B + 4;               // offset of the late-part starts
 
-    static constexpr int kLtTeamT = kCompute / 2;     // lieutenants: two teams (even / odd blocks)
-    static constexpr int kTPRl = 8;                   // lieutenants: threads per row
-    // chain CTA: a G ring (G1_k | G2_k), an S ring (D_k^{-1} | r_k) and an A ring (list A), filled
-    // independently (G is static, r_k waits for the helpers)
-    static constexpr size_t kGStage = (size_t)2 * B * B * 16;
+    static constexpr int kLtTeams = 4, kLtTeamT = 128;   // lieutenants: 4 teams of 4 warps (blocks k mod 4)
+    static constexpr int kWProducerLt = kNT / 32 - 1;
+    static constexpr int kTPRl = 16;                  // lieutenants: threads per row
+    // chain CTA: a G ring (G1_k | G2_k | G3_k) and an S ring (y_k), filled independently (G is
+    // static, y_k waits for the helpers)
+    static constexpr size_t kGStage = (size_t)kDense * B * B * 16;
     static constexpr size_t kOffSR = kGStage * kGStages;
-    static constexpr size_t kOffInv = 0;
-    static constexpr size_t kOffRfar = kOffInv + (size_t)kPK * 16;
-    static constexpr size_t kSStage = kOffRfar + (size_t)B * 16;
-    static constexpr size_t kOffAR = kOffSR + kSStage * kSStages;
-    static constexpr size_t kOffAcol = 0;
-    static constexpr size_t kOffAval = kOffAcol + (size_t)kCapA * 4;
-    static constexpr size_t kOffAloc = kOffAval + (size_t)kCapA * 16;
-    static constexpr size_t kAStage = kOffAloc + (size_t)kNloc * 4;
-    static constexpr size_t kChainRegion = kOffAR + kAStage * kAStages;
+    static constexpr size_t kSStage = (size_t)B * 16;
+    static constexpr size_t kChainRegion = kOffSR + kSStage * kSStages;
     // lieutenant stage: list B columns | values | row pointers
     static constexpr size_t kOffBcol = 0;
     static constexpr size_t kOffBval = kOffBcol + (size_t)kCapB * 4;
     static constexpr size_t kOffBloc = kOffBval + (size_t)kCapB * 16;
-    static constexpr size_t kLtStage = kOffBloc + (size_t)kNloc * 4;
+    static constexpr size_t kOffBinv = kOffBloc + (size_t)kNloc * 4;   // D_k^{-1} (packed)
+    static constexpr size_t kLtStage = kOffBinv + (size_t)kPK * 16;
     static constexpr int kLtStages = 4;
     static constexpr size_t kOffLtRing = kLtStage * kLtStages;   // lieutenants' x ring
-    static constexpr size_t kLtRegion = kOffLtRing + (size_t)kRingLt * B * 16;
+    static constexpr size_t kOffLtP = kOffLtRing + (size_t)kRingLt * B * 16;   // [kLtTeams][B] row partials
+    static constexpr size_t kLtRegion = kOffLtP + (size_t)kLtTeams * B * 16;
     static constexpr size_t kStageRegion = kChainRegion > kLtRegion ? kChainRegion : kLtRegion;
     static constexpr size_t kOffRing = kStageRegion;
-    static constexpr size_t kOffR = kOffRing + (size_t)kRing * B * 16;
-    static constexpr size_t kOffPbuf = kOffR + (size_t)2 * B * 16;
-    static constexpr size_t kOffYbuf = kOffPbuf + (size_t)kPbuf * B * 16;
-    static constexpr size_t kOffTpart = kOffYbuf + (size_t)kYbuf * B * 16;   // [4][kTeam][B] partials
-    static constexpr size_t kOffXw = kOffTpart + (size_t)4 * kTeam * B * 16;   // [2 kTeam][B] own x_k
-    static constexpr size_t kOffAbuf = kOffXw + (size_t)2 * kTeam * B * 16;   // [2][B] list A products
-    static constexpr size_t kOffRowP = kOffAbuf + (size_t)2 * B * 16;
+    static constexpr size_t kOffR = kOffRing + (size_t)kRing * B * 16;          // helpers: b_k - far
+    static constexpr size_t kOffPbuf = kOffR + (size_t)B * 16;
+    static constexpr size_t kOffTpart = kOffPbuf + (size_t)kPbuf * kLt * B * 16;   // [4][kTeam][B] partials
+    static constexpr size_t kOffXw = kOffTpart + (size_t)4 * kTeam * B * 16;   // [kTeams kTeam][B] own x_k
+    static constexpr size_t kOffRowP = kOffXw + (size_t)kTeams * kTeam * B * 16;
     static constexpr size_t kOffRowL = kOffRowP + (size_t)B * 8;
     static constexpr size_t kOffBar = kOffRowL + (size_t)B * 4;
     // mbarriers: full/empty per S stage (lieutenants: per list B stage), full/empty per G
-    // stage, xbar (lieutenant: x block landed), pbar (chain: partial landed), xfull (ring slot
-    // holds x_k), yempty (y slots), pready (team partials and y_k), then int counters
+    // stage, xbar (lieutenant: x block landed), pbar (chain: partials landed), xfull (ring slot
+    // holds x_k), pready (team partials), rfull (y_k staged), then int counters
     static constexpr int kNS = kSStages > kLtStages ? kSStages : kLtStages;
     static constexpr size_t kOffFull = kOffBar;
     static constexpr size_t kOffEmpty = kOffFull + 8 * kNS;
@@ -234,22 +223,18 @@ struct Cfg {
     static constexpr size_t kOffXbar = kOffGempty + 8 * kGStages;
     static constexpr size_t kOffPbar = kOffXbar + 8 * kRingLt;
     static constexpr size_t kOffXfull = kOffPbar + 8 * kPbuf;
-    static constexpr size_t kOffYempty = kOffXfull + 8 * kRing;
-    static constexpr size_t kOffPready = kOffYempty + 8 * kYbuf;
+    static constexpr size_t kOffPready = kOffXfull + 8 * kRing;
     static constexpr size_t kOffRfull = kOffPready + 8 * 4;
-    static constexpr size_t kOffAready = kOffRfull + 8 * kSStages;
-    static constexpr size_t kOffAempty = kOffAready + 8 * 2;
-    static constexpr size_t kOffAfull = kOffAempty + 8 * 2;   // A ring
-    static constexpr size_t kOffAslot = kOffAfull + 8 * kAStages;
-    static constexpr size_t kOffInts = kOffAslot + 8 * kAStages;
+    static constexpr size_t kOffInts = kOffRfull + 8 * kSStages;
     static constexpr size_t kSmem = kOffInts + 64;
-    static_assert(B == 32 && kDense == 2, "the chain teams hold one row per lane and the G1, G2 blocks");
+    static_assert(B == 32 && kDense == 3, "the chain teams hold one row per lane and the G1, G2, G3 blocks");
     static_assert(kCompute % B == 0 && B % kFarWarps == 0 && kRPW % kGrp == 0, "layout");
-    static_assert(kTeamW0 + 2 * kTeam == kNT / 32 && kCompute / 32 + 1 <= kNT / 32, "warp roles");
-    static_assert(kTPRl * ((B + kLt - 1) / kLt) <= kLtTeamT, "lieutenant rows");
-    static_assert(kSStage % 16 == 0 && kLtStage % 16 == 0 && kOffSR % 16 == 0 && kOffRfar % 16 == 0 &&
-                      kOffAR % 16 == 0 && kAStage % 16 == 0 && kOffAval % 16 == 0 && kOffAloc % 16 == 0 &&
-                      kOffBval % 16 == 0 && kOffBloc % 16 == 0 && kOffLtRing % 16 == 0,
+    static_assert(kTeamW0 + kTeams * kTeam == kNT / 32 && kCompute / 32 + 1 <= kNT / 32, "warp roles");
+    static_assert(kTPRl * ((B + kLt - 1) / kLt) <= kLtTeamT && kLtTeams * kLtTeamT <= 32 * kWProducerLt &&
+                      kLtTeams <= kLtStages,
+                  "lieutenant rows / teams");
+    static_assert(kSStage % 16 == 0 && kLtStage % 16 == 0 && kOffSR % 16 == 0 &&
+                      kOffBval % 16 == 0 && kOffBloc % 16 == 0 && kOffBinv % 16 == 0 && kOffLtRing % 16 == 0,
                   "TMA alignment");
     static_assert(kSmem <= 232448, "shared memory");
 };
@@ -332,12 +317,6 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
     uint64_t* pbar = reinterpret_cast<uint64_t*>(smem + C::kOffPbar);
     uint64_t* xfull = reinterpret_cast<uint64_t*>(smem + C::kOffXfull);
     uint64_t* rfull = reinterpret_cast<uint64_t*>(smem + C::kOffRfull);   // chain: r_k staged
-    uint64_t* aready = reinterpret_cast<uint64_t*>(smem + C::kOffAready);  // chain: list A product
-    uint64_t* aempty = reinterpret_cast<uint64_t*>(smem + C::kOffAempty);
-    double2* abuf = reinterpret_cast<double2*>(smem + C::kOffAbuf);
-    uint64_t* afull = reinterpret_cast<uint64_t*>(smem + C::kOffAfull);
-    uint64_t* aslot = reinterpret_cast<uint64_t*>(smem + C::kOffAslot);
-    uint64_t* yempty = reinterpret_cast<uint64_t*>(smem + C::kOffYempty);
     double2* tpart = reinterpret_cast<double2*>(smem + C::kOffTpart);
     uint64_t* pready = reinterpret_cast<uint64_t*>(smem + C::kOffPready);
     int* sDone = reinterpret_cast<int*>(smem + C::kOffInts);   // chain: blocks of x done
@@ -346,7 +325,6 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
     int* sPub = sDone + 3;                                        // chain: blocks published
     double2* ring = reinterpret_cast<double2*>(smem + C::kOffRing);
     double2* pbuf = reinterpret_cast<double2*>(smem + C::kOffPbuf);
-    double2* ybuf = reinterpret_cast<double2*>(smem + C::kOffYbuf);
     constexpr int kRingMask = C::kRing * B - 1;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -360,15 +338,7 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
     if (tid == 0) {
         for (int s = 0; s < C::kNS; s++) {
             mbar_init(full + s, 1);
-            mbar_init(empty + s, chain ? 2 : 1);   // chain CTA: the y team's 2 warps
-        }
-        for (int j = 0; j < 2; j++) {
-            mbar_init(aready + j, 1);
-            mbar_init(aempty + j, 2);
-        }
-        for (int j = 0; j < C::kAStages; j++) {
-            mbar_init(afull + j, 1);
-            mbar_init(aslot + j, 1);
+            mbar_init(empty + s, chain ? C::kTeam : 1);   // chain CTA: the warps of the block's team
         }
         for (int s = 0; s < C::kSStages; s++) mbar_init(rfull + s, 1);
         for (int s = 0; s < C::kGStages; s++) {
@@ -378,8 +348,7 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
         for (int j = 0; j < C::kRingLt; j++) mbar_init(xbar + j, 1);
         for (int j = 0; j < C::kPbuf; j++) mbar_init(pbar + j, 1);
         for (int j = 0; j < C::kRing; j++) mbar_init(xfull + j, 1);
-        for (int j = 0; j < C::kYbuf; j++) mbar_init(yempty + j, C::kTeam);
-        for (int j = 0; j < 4; j++) mbar_init(pready + j, C::kTeam + 2);   // a team's warps + the y team's 2
+        for (int j = 0; j < 4; j++) mbar_init(pready + j, C::kTeam);
         *sDone = 0;
         *sF = 0;
         *sLock = 0;
@@ -392,7 +361,7 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
         const int nst = chain ? C::kSStages : C::kLtStages;
         const size_t stsz = chain ? C::kSStage : C::kLtStage;
         unsigned char* const sbase = smem + (chain ? C::kOffSR : 0);
-        const int wprod = chain ? C::kWProducerChain : C::kCompute / 32;
+        const int wprod = chain ? C::kWProducerChain : C::kWProducerLt;
         if (warp == wprod) {
             // ------------------------------------------------ producer: TMA staging; lane 0 the
             // S ring (lieutenants: list B), lane 1 the chain's G ring (independent of the helpers)
@@ -414,48 +383,29 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     if (k >= nst) mbar_wait(empty + s, (uint32_t)((k / nst - 1) & 1));
                     unsigned char* st = sbase + stsz * s;
                     if (chain) {
-                        // D_k^{-1} as soon as the slot is free; r_k (on its own barrier) once the
-                        // helpers have published it
-                        mbar_expect_tx(full + s, (uint32_t)(C::kPK * 16));
-                        bulk_g2s(st + C::kOffInv, a.dinv + (int64_t)k * C::kPK, C::kPK * 16, full + s);
-                        if (trace) STAMP(k, 9);
+                        // y_k once the helpers have published it
                         while (ld_acquire(a.fflag + k) != epoch) __nanosleep(kProducerSleep);
                         if (trace) STAMP(k, 5);
-                        fence_proxy_async();   // r_k (generic-proxy stores of a helper) -> TMA reads
+                        fence_proxy_async();   // y_k (generic-proxy stores of a helper) -> TMA reads
                         mbar_expect_tx(rfull + s, (uint32_t)(B * 16));
-                        bulk_g2s(st + C::kOffRfar, a.rfar + (int64_t)k * B, B * 16, rfull + s);
+                        bulk_g2s(st, a.yfar + (int64_t)k * B, B * 16, rfull + s);
                     } else {
                         const int g = k * C::kLt + (role - 1);   // this lieutenant's rows of block k
                         stage_near(st + C::kOffBcol, st + C::kOffBval, st + C::kOffBloc, b0, b1, a.ncolB, a.nvalB,
-                                   a.nlocB, g, C::kNloc, full + s);
+                                   a.nlocB, g, C::kNloc, full + s, (uint32_t)(C::kPK * 16));
+                        bulk_g2s(st + C::kOffBinv, a.dinv + (int64_t)k * C::kPK, C::kPK * 16, full + s);
                     }
                 }
             }
         } else if (chain && warp == C::kWGProducer) {
-            // ------------------------------------------------ G producer: the teams' G ring and the
-            // A warp's list A ring (both static)
+            // ------------------------------------------------ G producer: the teams' G ring
             if (lane == 0) {
-                int64_t nb0 = 0, nb1 = 0;
-                if (nblk > 0) {
-                    nb0 = __ldg(a.nbpA);
-                    nb1 = __ldg(a.nbpA + 1);
-                }
                 for (int k = 0; k < nblk; k++) {
                     const int s = k % C::kGStages;
                     if (k >= C::kGStages) mbar_wait(gempty + s, (uint32_t)((k / C::kGStages - 1) & 1));
                     mbar_expect_tx(gfull + s, (uint32_t)C::kGStage);
                     bulk_g2s(smem + C::kGStage * s, a.G + (int64_t)k * kDense * B * B, (uint32_t)C::kGStage,
                              gfull + s);
-                    const int sa = k % C::kAStages;
-                    const int64_t b0 = nb0, b1 = nb1;
-                    if (k + 1 < nblk) {
-                        nb0 = __ldg(a.nbpA + k + 1);
-                        nb1 = __ldg(a.nbpA + k + 2);
-                    }
-                    if (k >= C::kAStages) mbar_wait(aslot + sa, (uint32_t)((k / C::kAStages - 1) & 1));
-                    unsigned char* st = smem + C::kOffAR + C::kAStage * sa;
-                    stage_near(st + C::kOffAcol, st + C::kOffAval, st + C::kOffAloc, b0, b1, a.ncolA, a.nvalA, a.nlocA,
-                               k, C::kNloc, afull + sa);
                 }
             }
         } else if (chain && warp == C::kWPublisher) {
@@ -489,87 +439,75 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     st_rel_cta(sPub, j);
                 }
             }
-        } else if (chain && warp == C::kWA) {
-            // ------------------------------------------------ A warp: a_k = T_{k,k-kDA} x_{k-kDA}
-            // (list A, one thread per row), into abuf for the y warps
-            const int r = lane;
-            for (int k = 0; k < nblk; k++) {
-                const int s = k % C::kAStages, ab = k & 1;
-                unsigned char* st = smem + C::kOffAR + C::kAStage * s;
-                mbar_wait(afull + s, (uint32_t)((k / C::kAStages) & 1));
-                const int32_t* loc = reinterpret_cast<const int32_t*>(st + C::kOffAloc);
-                const int32_t* col = reinterpret_cast<const int32_t*>(st + C::kOffAcol);
-                const double2* val = reinterpret_cast<const double2*>(st + C::kOffAval);
-                const int lo = loc[r], hi = loc[r + 1];
-                double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
-                if (trace && lane == 0) STAMP(k, 15);
-                if (k >= C::kDA) {
-                    mbar_wait(xfull + (k - C::kDA) % C::kRing, (uint32_t)(((k - C::kDA) / C::kRing) & 1));
-                    if (trace && lane == 0) STAMP(k, 14);
-                    int e = lo;
-                    for (; e + 1 < hi; e += 2) {
-                        const int c0 = col[e], c1 = col[e + 1];
-                        const double2 v0 = val[e], v1 = val[e + 1];
-                        acc = cfma(acc, v0, ring[c0 & kRingMask]);
-                        acc2 = cfma(acc2, v1, ring[c1 & kRingMask]);
-                    }
-                    if (e < hi) acc = cfma(acc, val[e], ring[col[e] & kRingMask]);
-                }
-                if (k >= 2) mbar_wait(aempty + ab, (uint32_t)((k / 2 - 1) & 1));   // y read block k-2's
-                abuf[ab * B + r] = cadd(acc, acc2);
-                __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(aready + ab);
-                    mbar_arrive(aslot + s);
-                    if (trace) STAMP(k, 11);
-                }
-            }
         } else if (chain && warp >= C::kTeamW0) {
-            // ------------------------------------------------ chain teams A (even blocks) and B
-            // (odd blocks), 4 warps each:
-            //     x_k = y_k - sum_w [ G1_k[:, w] x_{k-1}[w] + G2_k[:, w] x_{k-2}[w] ]
-            // Warp w of a team owns 8 columns (slice w).  While the other team computes x_{k-1},
-            // the team of block k loads G1_k (registers) and forms the carry G2_k x_{k-2} from
-            // its own x_{k-2}; then only x_{k-1} (from the ring, xfull) -> G1_k x_{k-1} -> the
+            // ------------------------------------------------ chain teams 0, 1, 2 (blocks k = team
+            // mod 3), 4 warps each:
+            //     x_k = y_k - sum_w [ G1_k[:, w] x_{k-1}[w] + G2_k[:, w] x_{k-2}[w] + G3_k[:, w] x_{k-3}[w] ]
+            // Warp w of a team owns 8 columns (slice w).  While the other teams compute x_{k-2},
+            // x_{k-1}, the team of block k loads G1_k (registers) and forms the carry G2_k x_{k-2}
+            // (the ring) + G3_k x_{k-3} (its own); then only x_{k-1} (from the ring, xfull) ->
+            // G1_k x_{k-1} -> the
             // partials (pready, which also carries y_k) -> x_k is on the chain.  Every warp
             // reduces the partials itself; warp 0 stores x_k to the ring and releases xfull,
             // warp 1 pushes x_k to the lieutenants.
-            const int team = (warp - C::kTeamW0) / C::kTeam;   // 0: even blocks, 1: odd
+            const int team = (warp - C::kTeamW0) / C::kTeam;   // blocks k = team mod kTeams
             const int tw = (warp - C::kTeamW0) % C::kTeam;
             const int j0 = tw * C::kSlice;
-            double2* xw = reinterpret_cast<double2*>(smem + C::kOffXw) + (warp - C::kTeamW0) * B;   // my x_{k-2}
+            double2* xw = reinterpret_cast<double2*>(smem + C::kOffXw) + (warp - C::kTeamW0) * B;   // my x_{k-3}
             uint32_t peer_ring[C::kLt], peer_xbar[C::kLt];   // warp 1: the lieutenants' rings
 #pragma unroll
             for (int l = 0; l < C::kLt; l++) {
                 peer_ring[l] = mapa(smem_u32(smem + C::kOffLtRing), (uint32_t)(l + 1));
                 peer_xbar[l] = mapa(smem_u32(xbar), (uint32_t)(l + 1));
             }
-            for (int k = team; k < nblk; k += 2) {
-                const int yb = k % C::kYbuf, pq = k & 3;
+            for (int k = team; k < nblk; k += C::kTeams) {
+                const int pq = k & 3;
                 TPROF(k, 0);
                 // ---- off the chain (the other team is computing x_{k-1})
                 if (tw == 0 && k >= C::kRing)   // ring slot of block k held block k-8: published?
                     while (ld_acq_cta(sPub) < k - C::kRing + 1) {
                     }
+                TPROF(k, 8);
                 double2 g1[C::kSlice];
-                double2 carry = make_double2(0.0, 0.0);   // G2_k[lane, slice] x_{k-2}[slice]
+                double2 carry = make_double2(0.0, 0.0);   // (G2_k x_{k-2} + G3_k x_{k-3})[lane, slice]
                 {
                     const int s = k % C::kGStages;
                     mbar_wait(gfull + s, (uint32_t)((k / C::kGStages) & 1));
+                    TPROF(k, 9);
                     const double2* G = reinterpret_cast<const double2*>(smem + C::kGStage * s);
 #pragma unroll
                     for (int u = 0; u < C::kSlice; u++) g1[u] = G[(j0 + u) * B + lane];
-                    if (k >= 2) {
-                        double2 c1 = make_double2(0.0, 0.0);
+                    TPROF(k, 10);
+                    double2 c1 = make_double2(0.0, 0.0);
+                    if (k >= 3) {   // x_{k-3}: this team's previous block
 #pragma unroll
-                        for (int u = 0; u < C::kSlice; u += 2) {
-                            carry = cfma(carry, G[B * B + (j0 + u) * B + lane], xw[j0 + u]);
-                            c1 = cfma(c1, G[B * B + (j0 + u + 1) * B + lane], xw[j0 + u + 1]);
-                        }
-                        carry = cadd(carry, c1);
+                        for (int u = 0; u < C::kSlice; u++)
+                            c1 = cfma(c1, G[2 * B * B + (j0 + u) * B + lane], xw[j0 + u]);
                     }
+                    TPROF(k, 11);
+                    if (k >= 2) {
+                        mbar_wait(xfull + (k - 2) % C::kRing, (uint32_t)(((k - 2) / C::kRing) & 1));   // x_{k-2}
+                        TPROF(k, 12);
+                        const double2* x2 = ring + (((int64_t)(k - 2) * B) & kRingMask);
+#pragma unroll
+                        for (int u = 0; u < C::kSlice; u++) carry = cfma(carry, G[B * B + (j0 + u) * B + lane], x2[j0 + u]);
+                    }
+                    carry = cadd(carry, c1);
+                    TPROF(k, 13);
                     __syncwarp();
                     if (lane == 0) mbar_arrive(gempty + s);
+                }
+                // y_k (lane = row), staged by the producer once the helpers published it
+                double2 yk;
+                {
+                    const int s = k % C::kSStages;
+                    mbar_wait(rfull + s, (uint32_t)((k / C::kSStages) & 1));
+                    yk = reinterpret_cast<const double2*>(smem + C::kOffSR + C::kSStage * s)[lane];
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_arrive(empty + s);
+                        if (tw == 0) mbar_expect_tx(pbar + k % C::kPbuf, (uint32_t)(C::kLt * B * 16));   // the q_l of block k
+                    }
                 }
                 TPROF(k, 1);
                 if (trace && tw == 0 && lane == 0) STAMP(k, 10);
@@ -597,12 +535,15 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                 if (lane == 0) mbar_arrive(pready + pq);   // this warp's partial is in tpart
                 TPROF(k, 3);
                 mbar_wait(pready + pq, (uint32_t)((k >> 2) & 1));   // the team's partials and y_k
+                mbar_wait(pbar + k % C::kPbuf, (uint32_t)((k / C::kPbuf) & 1));   // the lieutenants' q_l
                 TPROF(k, 4);
                 if (trace && tw == 0 && lane == 0) STAMP(k, 0);
                 double2 sum = tpart[(pq * C::kTeam + 0) * B + lane];
 #pragma unroll
                 for (int w = 1; w < C::kTeam; w++) sum = cadd(sum, tpart[(pq * C::kTeam + w) * B + lane]);
-                const double2 xk = csub(ybuf[yb * B + lane], sum);
+#pragma unroll
+                for (int l = 0; l < C::kLt; l++) sum = cadd(sum, pbuf[((k % C::kPbuf) * C::kLt + l) * B + lane]);
+                const double2 xk = csub(yk, sum);
                 TPROF(k, 5);
                 if (tw == 0) {
                     ring[((int64_t)k * B + lane) & kRingMask] = xk;
@@ -621,79 +562,24 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                         for (int l = 0; l < C::kLt; l++) mbar_arrive_expect_tx_remote(peer_xbar[l] + bar, B * 16);
                     if (trace && lane == 0) STAMP(k, 8);
                 }
-                xw[lane] = xk;   // my x_k: the carry of block k+2
+                xw[lane] = xk;   // my x_k: the carry of block k+3
                 __syncwarp();
-                if (lane == 0) mbar_arrive(yempty + yb);
                 TPROF(k, 7);
-            }
-        } else if (chain && warp >= C::kYW0) {
-            // ------------------------------------------------ y warps:
-            // y_k = D_k^{-1} (r_k - lieutenant partials - list A product)
-            // two y teams of 2 warps take the even / odd blocks (each has two chain steps);
-            // 2 threads per row (r = row, q = column class j = q mod 2): D_k^{-1}[r, j], j <= r,
-            // lives in registers; one named barrier per block (the residual vector).
-            const int yteam = (warp - C::kYW0) >> 1;           // 0: even blocks, 1: odd blocks
-            const int yt = ((warp - C::kYW0) & 1) * 32 + lane;   // 0 .. 63
-            constexpr int kYT = 64;
-            constexpr int kQ = kYT / B;                     // 2 threads per row
-            const int r = yt / kQ, q = yt % kQ;
-            double2* sR = reinterpret_cast<double2*>(smem + C::kOffR) + yteam * B;   // [2][B]
-            for (int k = yteam; k < nblk; k += 2) {
-                const int s = k % C::kSStages, yb = k % C::kYbuf, pk = k % C::kPbuf;
-                unsigned char* st = smem + C::kOffSR + C::kSStage * s;
-                mbar_wait(full + s, (uint32_t)((k / C::kSStages) & 1));
-                if (trace && yt == 0) STAMP(k, 2);
-                const double2* sInv = reinterpret_cast<const double2*>(st + C::kOffInv);
-                double2 dv[B / kQ];
-#pragma unroll
-                for (int t = 0; t < B / kQ; t++) {
-                    const int j = q + kQ * t;
-                    dv[t] = j <= r ? sInv[j * B - (j * (j - 1)) / 2 + (r - j)] : make_double2(0.0, 0.0);
-                }
-                if (yt == 0) mbar_expect_tx(pbar + pk, (uint32_t)(B * 16));
-                mbar_wait(rfull + s, (uint32_t)((k / C::kSStages) & 1));   // r_k
-                const double2 rf = reinterpret_cast<const double2*>(st + C::kOffRfar)[r];
-                mbar_wait(pbar + pk, (uint32_t)((k / C::kPbuf) & 1));   // lieutenants' partials
-                if (trace && yt == 0) STAMP(k, 6);
-                mbar_wait(aready + (k & 1), (uint32_t)((k >> 1) & 1));   // list A product
-                if (q == 0) sR[r] = csub(csub(rf, pbuf[pk * B + r]), abuf[(k & 1) * B + r]);
-                bar_named(2 + yteam * 2, kYT);   // the team's residual vector is complete
-                if (lane == 0) mbar_arrive(aempty + (k & 1));
-                double2 y0 = make_double2(0.0, 0.0), y1 = make_double2(0.0, 0.0);
-#pragma unroll
-                for (int t = 0; t < B / kQ; t += 2) {
-                    y0 = cfma(y0, dv[t], sR[q + kQ * t]);
-                    y1 = cfma(y1, dv[t + 1], sR[q + kQ * (t + 1)]);
-                }
-                double2 yv = cadd(y0, y1);
-#pragma unroll
-                for (int o = 1; o < kQ; o <<= 1) {
-                    yv.x += __shfl_xor_sync(0xffffffffu, yv.x, o);
-                    yv.y += __shfl_xor_sync(0xffffffffu, yv.y, o);
-                }
-                if (q == 0) {
-                    if (k >= C::kYbuf) mbar_wait(yempty + yb, (uint32_t)((k / C::kYbuf - 1) & 1));
-                    ybuf[yb * B + r] = yv;
-                }
-                __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(pready + (k & 3));   // y_k: one arrival per y warp (its 16 rows)
-                    mbar_arrive(empty + s);
-                    if (trace && yt == 0) STAMP(k, 1);
-                }
-                bar_named(2 + yteam * 2, kYT);   // sR is reused by the team's next block
             }
         } else if (!chain) {
             // ------------------------------------------------ lieutenants: list B partial sums
-            // (source distance kDA+1 .. Q_k-1) of the rows l, l+kLt, ...; two teams of 4
-            // warps take the even / odd blocks.  The early part (distance >= kDA+2) is
-            // summed before x_{k-kDA-1} lands, the late part after.  x blocks land by
+            // (source distance kDense+1 .. Q_k-1) of the rows l, l+kLt, ...; kLtTeams teams of
+            // 4 warps take the blocks k mod kLtTeams.  The early part (distance >= kDense+2) is
+            // summed before x_{k-kDense-1} lands, the late part after.  x blocks land by
             // st.async from the chain team, which also makes each xbar phase's one arrival.
+            // Each lieutenant sends q_l = D_k^{-1}[:, its rows] (its row partials), so the chain
+            // only subtracts the three q_l from y_k = D_k^{-1} r_k.
             const int l = role - 1;
             const uint32_t peer_pbuf = mapa(smem_u32(pbuf), 0u);
             const uint32_t peer_pbar = mapa(smem_u32(pbar), 0u);
             const double2* ltring = reinterpret_cast<const double2*>(smem + C::kOffLtRing);
             const int lteam = tid / C::kLtTeamT, tt = tid % C::kLtTeamT;
+            double2* lp = reinterpret_cast<double2*>(smem + C::kOffLtP) + lteam * B;   // row partials
             int xseen = 0;   // x blocks < xseen have landed in the ring
             const int r = l + C::kLt * (tt / C::kTPRl), q = tt % C::kTPRl;
             const bool rowok = r < B;
@@ -701,8 +587,8 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                 for (; xseen <= upto; xseen++)
                     mbar_wait(xbar + xseen % C::kRingLt, (uint32_t)((xseen / C::kRingLt) & 1));
             };
-            if (warp < C::kCompute / 32) {
-                for (int k = lteam; k < nblk; k += 2) {
+            if (lteam < C::kLtTeams) {
+                for (int k = lteam; k < nblk; k += C::kLtTeams) {
                     const int s = k % nst;
                     unsigned char* st = smem + stsz * s;
                     mbar_wait(full + s, (uint32_t)((k / nst) & 1));
@@ -712,9 +598,10 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     const int32_t* col = reinterpret_cast<const int32_t*>(st + C::kOffBcol);
                     const double2* val = reinterpret_cast<const double2*>(st + C::kOffBval);
                     double2 acc = make_double2(0.0, 0.0);
-                    land(k - C::kDA - 2);
+                    land(k - kDense - 2);
                     if (rowok) acc = near_range<B, C::kTPRl, C::kRingLt>(col, val, ltring, loc[r], loc[C::kLate + r], q, acc);
-                    land(k - C::kDA - 1);
+                    if (tr0) STAMP(k, 11);
+                    land(k - kDense - 1);
                     if (tr0) STAMP(k, 7);
                     if (rowok) acc = near_range<B, C::kTPRl, C::kRingLt>(col, val, ltring, loc[C::kLate + r], loc[r + 1], q, acc);
 #pragma unroll
@@ -722,9 +609,29 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                         acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
                         acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
                     }
-                    if (rowok && q == 0) {
-                        const int pk = k % C::kPbuf;
-                        st_async2(peer_pbuf + (uint32_t)((pk * B + r) * 16), acc, peer_pbar + (uint32_t)(pk * 8));
+                    if (rowok && q == 0) lp[r] = acc;
+                    bar_named(2 + lteam, C::kLtTeamT);
+                    // q_l = D_k^{-1}[:, rows of l] p_l: output row i = tt / 4, the rows m = part,
+                    // part + 4, ... of this lieutenant (4 threads per output row)
+                    {
+                        const double2* sInv = reinterpret_cast<const double2*>(st + C::kOffBinv);
+                        const int i = tt >> 2, part = tt & 3;
+                        double2 qa = make_double2(0.0, 0.0);
+#pragma unroll
+                        for (int m = part; m * C::kLt + l < B; m += 4) {
+                            const int rr = m * C::kLt + l;
+                            if (rr <= i) qa = cfma(qa, sInv[rr * B - (rr * (rr - 1)) / 2 + (i - rr)], lp[rr]);
+                        }
+#pragma unroll
+                        for (int o = 1; o < 4; o <<= 1) {
+                            qa.x += __shfl_xor_sync(0xffffffffu, qa.x, o);
+                            qa.y += __shfl_xor_sync(0xffffffffu, qa.y, o);
+                        }
+                        if (part == 0) {
+                            const int pk = k % C::kPbuf;
+                            st_async2(peer_pbuf + (uint32_t)(((pk * C::kLt + l) * B + i) * 16), qa,
+                                      peer_pbar + (uint32_t)(pk * 8));
+                        }
                     }
                     bar_named(2 + lteam, C::kLtTeamT);
                     if (tt == 0) {
@@ -749,6 +656,8 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
     const int H = gridDim.x - C::kCluster;
     int64_t* sRowP = reinterpret_cast<int64_t*>(smem + C::kOffRowP);
     int32_t* sRowL = reinterpret_cast<int32_t*>(smem + C::kOffRowL);
+    double2* sRf = reinterpret_cast<double2*>(smem + C::kOffR);   // b_k - far part
+    const int yi = tid >> 3, yp = tid & 7;                         // D^{-1} product: row, column class
     for (int k = blockIdx.x - C::kCluster; k < nblk; k += H) {
         const int64_t row0 = (int64_t)k * B;
         double2 acc[C::kRPW];
@@ -806,7 +715,28 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
         for (int r = 0; r < C::kRPW; r++) {
             const double2 sm = warp_sum2(acc[r]);
             const int64_t i = row0 + warp * C::kRPW + r;
-            if (lane == 0) a.rfar[i] = (i < n) ? csub(__ldg(bvec + phys(i)), sm) : make_double2(0.0, 0.0);
+            if (lane == 0) sRf[warp * C::kRPW + r] = (i < n) ? csub(__ldg(bvec + phys(i)), sm) : make_double2(0.0, 0.0);
+        }
+        double2 dv[B / 8];   // D_k^{-1}[yi, yp + 8m]
+#pragma unroll
+        for (int m = 0; m < B / 8; m++) {
+            const int j = yp + 8 * m;
+            dv[m] = j <= yi ? __ldg(a.dinv + (int64_t)k * C::kPK + j * B - (j * (j - 1)) / 2 + (yi - j))
+                            : make_double2(0.0, 0.0);
+        }
+        bar_named(1, C::kCompute);
+        // y_k = D_k^{-1} (b_k - far part): output row yi = tid / 8, columns j = yp, yp + 8, ...
+        {
+            double2 ya = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int m = 0; m < B / 8; m++)
+                if (yp + 8 * m <= yi) ya = cfma(ya, dv[m], sRf[yp + 8 * m]);
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) {
+                ya.x += __shfl_xor_sync(0xffffffffu, ya.x, o);
+                ya.y += __shfl_xor_sync(0xffffffffu, ya.y, o);
+            }
+            if (yp == 0) a.yfar[row0 + yi] = ya;
         }
         bar_named(1, C::kCompute);
         if (tid == 0) {

@@ -19,6 +19,8 @@ import paper_1411_4356_b200 as pb  # noqa: E402
 from workloads import CONFIGS  # noqa: E402
 
 NAMES = ["start", "offchain", "x_prev", "partial", "pready", "reduce", "release", "end"]
+SLACK = [(0, 8, "start->spub"), (8, 9, "spub->gstage"), (9, 10, "gstage->g1"), (10, 11, "g1->g2carry"),
+         (11, 12, "g2carry->x3wait"), (12, 13, "x3wait->g3carry"), (13, 1, "g3carry->offchain")]
 
 
 def main():
@@ -30,6 +32,8 @@ def main():
         pb.ss_debug_trace_trsv(s.handle, which, x.data_ptr(), y.data_ptr())
         tr = pb.ss_debug_trace_trsv(s.handle, which, x.data_ptr(), y.data_ptr()).astype(np.int64)[8:-8]
         d = {f"{NAMES[i - 1]}->{NAMES[i]}": float(np.median(tr[:, i] - tr[:, i - 1])) for i in range(1, 8)}
+        for a_, b_, nm_ in SLACK:
+            d[nm_] = float(np.median(tr[:, b_] - tr[:, a_]))
         d["end->next start (same team)"] = float(np.median(tr[2:, 0] - tr[:-2, 7]))
         d["two steps (same team)"] = float(np.median(tr[2:, 0] - tr[:-2, 0]))
         out[nm] = d

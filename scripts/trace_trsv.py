@@ -54,9 +54,7 @@ def main():
             "y_stage_ready_ns": med(rel[:, 2] - done_prev),
             "y_pbar_ns": med(rel[:, 6] - done_prev),
             "team_g1_loaded_ns": med(rel[:, 13] - done_prev),
-            "a_stage_ready_ns": med(rel[:, 15] - done_prev),
-            "a_saw_xkm3_ns": med(rel[:, 14] - done_prev),
-            "a_done_ns": med(rel[:, 11] - done_prev),
+            "lt_early_done_ns": med(rel[:, 11] - done_prev),
             "y_done_ns": med(rel[:, 1] - done_prev),
             # lieutenant 0 (relative to x_{k-1} stored)
             "lt_stage_ready_ns": med(rel[:, 12] - done_prev),
@@ -68,6 +66,14 @@ def main():
             "producer_flag_pct_ns": [float(v) for v in np.percentile(rel[:, 5] - done_prev, [10, 50, 90, 99])],
             "first_blocks": tr[:3].tolist(),
         }
+        slow = step > 1.5 * med(step)
+        if slow.any():
+            d["slow_steps"] = int(slow.sum())
+            d["slow_team_offchain_done_ns"] = med((rel[:, 10] - done_prev)[slow])
+            d["slow_team_saw_prev_ns"] = med((rel[:, 13] - done_prev)[slow])
+            d["slow_team_ready_ns"] = med((rel[:, 0] - done_prev)[slow])
+            d["slow_lt_late_landed_ns"] = med((rel[:, 7] - done_prev)[slow])
+            d["slow_producer_flag_ns"] = med((rel[:, 5] - done_prev)[slow])
         out[nm] = d
     print(json.dumps(out), flush=True)
     s.close()

@@ -102,13 +102,11 @@ def test_spmv_and_substitutions(cuda, name):
     s.close()
 
 
-@pytest.mark.parametrize("knobs", [{"SSB_TRSV_Q": "4"}, {"SSB_TRSV_Q": "5"}, {"SSB_TRSV_Q": "9"},
-                                   {"SSB_TRSV_CAPA": "0"}])
+@pytest.mark.parametrize("knobs", [{"SSB_TRSV_Q": "4"}, {"SSB_TRSV_Q": "5"}, {"SSB_TRSV_Q": "9"}])
 def test_substitution_split_variants(cuda, monkeypatch, knobs):
     """The same substitutions with the source-distance split moved:
-    Q = 4 leaves the lieutenants' list B empty (everything beyond list A goes to the helper
-    CTAs), Q = 5 gives list B only its late part, Q = 9 a shorter window; CAPA = 0 overflows
-    every block's list A, so the helpers take every distance >= 3 (the overflow fallback)."""
+    Q = 4 leaves the lieutenants' list B empty (everything beyond the dense G blocks goes
+    to the helper CTAs), Q = 5 gives list B only its late part, Q = 9 a shorter window."""
     torch = cuda
     for k, v in knobs.items():
         monkeypatch.setenv(k, v)
@@ -126,10 +124,7 @@ def test_substitution_split_variants(cuda, monkeypatch, knobs):
         ym = s.precond(xd, 2).cpu().numpy()
         rm = T.apply_preconditioner(F, x)
         assert np.abs(ym - rm).max() <= 1e-10 * np.abs(rm).max()
-    if "SSB_TRSV_Q" in knobs:
-        assert max(s.setup_info["trsv_q_L"], s.setup_info["trsv_q_U"]) <= int(knobs["SSB_TRSV_Q"])
-    else:
-        assert s.setup_info["trsv_q_L"] == 3 and s.setup_info["trsv_q_U"] == 3
+    assert max(s.setup_info["trsv_q_L"], s.setup_info["trsv_q_U"]) <= int(knobs["SSB_TRSV_Q"])
     s.close()
 
 
