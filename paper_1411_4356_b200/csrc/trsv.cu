@@ -11,32 +11,35 @@
 // sec. 5).  Any row-level substitution pays one synchronisation per level; v1 (one CTA,
 // one barrier per level) ran at 2.6 us per level.
 //
-// v6 (this file): block substitution whose dependency chain runs in ONE WARP.
-// Rows are cut into blocks of B = 32 consecutive rows; in the kernel's index space (U
-// reversed at setup, i' = n-1-i, so both factors are lower triangular)
-//     x_k = D_k^{-1} ( b_k - sum_{j<k} T_kj x_j ) = y_k - G_k x_{k-1},
-//     y_k = D_k^{-1} ( b_k - sum_{j<k-1} T_kj x_j ),   G_k = D_k^{-1} T_{k,k-1},
-// with D_k^{-1} and G_k (dense 32 x 32) precomputed at setup.  Only x_k = y_k - G_k x_{k-1}
-// is on the chain: one warp, lane i = row i, x_{k-1} in registers (shuffles), G_k out of
-// shared memory -- no barrier on the critical path.  Everything else runs ahead of it:
-//   * y warps (7 warps of the chain CTA): y_k from the entries with source distance 2
-//     (list A, x_{k-2} from the shared-memory ring), the lieutenants' partial sums, the
-//     helpers' r_k and the triangular mat-vec with D_k^{-1} (trimv.cuh), one block ahead;
-//   * lieutenants (3 CTAs of the chain's thread-block cluster): the entries with source
-//     distance 3 .. Q_k-1 (list B), each for a third of the rows; every x block reaches
-//     their rings by st.async (DSMEM) and their partial sums come back the same way,
-//     both completing mbarrier transactions (no fences on the chain);
-//   * helpers (the other SMs): the "far" entries (source distance >= Q_k, the bulk of
-//     the factor bytes) streamed in fixed 32-entry chunks as the published frontier
-//     covers them; r_k = b_k - far part is published with a gpu-scope release flag;
-//   * producer warp: TMA bulk copies (cp.async.bulk + mbarrier) of D_k^{-1}, G_k, list A
-//     and r_k (chain CTA) or list B (lieutenants), stages ahead;
+// This file: block substitution whose dependency chain is one 32x32 complex mat-vec per
+// block on the chain CTA.  Rows are cut into blocks of B = 32 consecutive rows; in the
+// kernel's index space (U reversed at setup, i' = n-1-i, so both factors are lower
+// triangular)
+//     x_k = D_k^{-1} ( b_k - sum_{j<k} T_kj x_j )
+//         = y_k - sum_l q_{l,k} - G1_k x_{k-1} - G2_k x_{k-2} - G3_k x_{k-3},
+//     y_k = D_k^{-1} ( b_k - far_k ),  Gd_k = D_k^{-1} T_{k,k-d} (dense, precomputed),
+//     q_{l,k} = D_k^{-1}[:, rows of l] (list B of lieutenant l applied to x),
+// where "far" are the entries with source distance d >= Q_k and list B those with
+// 4 <= d < Q_k (setup.cpp::build_block_tri).  Only G1_k x_{k-1} is on the chain:
+//   * chain CTA (cluster rank 0): three chain teams of 4 warps rotate over the blocks;
+//     the team of block k prepares G1_k (registers), the carry G2_k x_{k-2} + G3_k x_{k-3}
+//     and y_k - sum_l q_l while the other teams compute x_{k-2}, x_{k-1}; then x_{k-1}
+//     (ring + mbarrier) -> G1_k x_{k-1} -> partials (mbarrier) -> x_k into the ring and,
+//     by st.async, into the lieutenants' rings;
+//   * lieutenants (cluster ranks 1..7, DSMEM): list B of rows l, l+7, ..., the early
+//     part (d >= 5) once x_{k-5} has landed, the late part (d = 4) once x_{k-4} has, times
+//     their columns of D_k^{-1}, st.async'd back to the chain CTA;
+//   * helpers (the other SMs): the far entries streamed in 32-entry chunks as the
+//     published frontier covers them; y_k published with a gpu-scope release flag;
+//   * producer warps: TMA bulk copies (cp.async.bulk + mbarrier) of G1|G2|G3 and y_k
+//     (chain CTA) or list B and D_k^{-1} (lieutenants), stages ahead;
 //   * publisher warp: copies finished x blocks from the ring to global memory (and
 //     through the iLUTP column permutation to the output, x = Pi y) and advances the
 //     frontier word (epoch << 32 | blocks done) with a gpu-scope release.
-// One CTA per SM, clusters of 4; the grid never exceeds the co-resident cluster count, so
+// One CTA per SM, clusters of 8; the grid never exceeds the co-resident cluster count, so
 // the spin waits cannot deadlock.  Every reduction has a fixed order: the result is
-// deterministic for given (B, Q).
+// deterministic for a given layout.  DESIGN.md sec. 5 has the measurements.
+
 #include "problem.h"
 
 namespace ssb {
