@@ -114,28 +114,38 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {   //
         : "memory");
     return ok != 0;
 }
+// try_wait's suspend-time hint: a waiting thread may be parked (no issue slots) until the
+// phase completes or this many ns pass
+constexpr uint32_t kSuspendNs = 20000;
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
         "@!p bra WAIT_%=;\n"
         "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "r"(kSuspendNs)
         : "memory");
 }
 
 constexpr int kTrace = SS_TRACE_STAMPS;   // stamps per block when tracing (include/ss_b200.h)
 // STAMP: the ss_debug_trace_trsv stamps (%globaltimer).  Built with -DSSB_TEAM_PROF instead,
 // TPROF stamps clock64() at sub-steps of the chain team's warp 0 (scripts/trace_trsv.py --team).
-#ifdef SSB_TEAM_PROF
+#if defined(SSB_TEAM_PROF)
 #define STAMP(k, i) ((void)0)
 #define TPROF(k, i) \
     if (trace && tw == 0 && lane == 0) trace[(int64_t)(k) * kTrace + (i)] = clock64()
+#define LPROF(k, i) ((void)0)
+#elif defined(SSB_LT_PROF)   // the same for lieutenant 0's team thread 0
+#define STAMP(k, i) ((void)0)
+#define TPROF(k, i) ((void)0)
+#define LPROF(k, i) \
+    if (trace && tt == 0 && l == 0) trace[(int64_t)(k) * kTrace + (i)] = clock64()
 #else
 #define STAMP(k, i) (trace[(int64_t)(k) * kTrace + (i)] = gtime())
 #define TPROF(k, i) ((void)0)
+#define LPROF(k, i) ((void)0)
 #endif
 constexpr int kProducerSleep = 32;   // back-off of the producer polling a helper flag (ns)
 __device__ __forceinline__ unsigned long long gtime() {
@@ -189,7 +199,8 @@ struct Cfg {
 
     static constexpr int kLtTeams = 4, kLtTeamT = 128;   // lieutenants: 4 teams of 4 warps (blocks k mod 4)
     static constexpr int kWProducerLt = kNT / 32 - 1;
-    static constexpr int kTPRl = 16;                  // lieutenants: threads per row
+    static constexpr int kTPRl = 16;                  // lieutenants: threads per row (early part)
+    static constexpr int kTPRlate = 4;                //              and of them for the late part
     // chain CTA: a G ring (G1_k | G2_k | G3_k) and an S ring (y_k), filled independently (G is
     // static, y_k waits for the helpers)
     static constexpr size_t kGStage = (size_t)kDense * B * B * 16;
@@ -202,7 +213,7 @@ struct Cfg {
     static constexpr size_t kOffBloc = kOffBval + (size_t)kCapB * 16;
     static constexpr size_t kOffBinv = kOffBloc + (size_t)kNloc * 4;   // D_k^{-1} (packed)
     static constexpr size_t kLtStage = kOffBinv + (size_t)kPK * 16;
-    static constexpr int kLtStages = 4;
+    static constexpr int kLtStages = 6;
     static constexpr size_t kOffLtRing = kLtStage * kLtStages;   // lieutenants' x ring
     static constexpr size_t kOffLtP = kOffLtRing + (size_t)kRingLt * B * 16;   // [kLtTeams][B] row partials
     static constexpr size_t kLtRegion = kOffLtP + (size_t)kLtTeams * B * 16;
@@ -285,6 +296,33 @@ __device__ __forceinline__ double2 near_range(const int32_t* col, const double2*
         acc2 = cfma(acc2, v1, ring[c1 & kRingMask]);
     }
     if (e < hi) acc = cfma(acc, val[e], ring[col[e] & kRingMask]);
+    return cadd(acc, acc2);
+}
+
+// Entries [lo, hi) of one row summed by ONE thread, 4 at a time with predicated
+// (branch-free) loads, x from the ring.
+template <int B, int kRingBlocks>
+__device__ __forceinline__ double2 row_sum_1t(const int32_t* col, const double2* val, const double2* ring, int lo,
+                                              int hi, double2 acc) {
+    constexpr int kRingMask = kRingBlocks * B - 1;
+    double2 acc2 = make_double2(0.0, 0.0);
+    for (int e = lo; e < hi; e += 4) {
+        int c[4];
+        double2 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const bool ok = e + u < hi;
+            const int ee = ok ? e + u : lo;
+            c[u] = col[ee];
+            v[u] = val[ee];
+            v[u].x = ok ? v[u].x : 0.0;
+            v[u].y = ok ? v[u].y : 0.0;
+        }
+        acc = cfma(acc, v[0], ring[c[0] & kRingMask]);
+        acc2 = cfma(acc2, v[1], ring[c[1] & kRingMask]);
+        acc = cfma(acc, v[2], ring[c[2] & kRingMask]);
+        acc2 = cfma(acc2, v[3], ring[c[3] & kRingMask]);
+    }
     return cadd(acc, acc2);
 }
 
@@ -537,15 +575,17 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                 __syncwarp();
                 if (lane == 0) mbar_arrive(pready + pq);   // this warp's partial is in tpart
                 TPROF(k, 3);
-                mbar_wait(pready + pq, (uint32_t)((k >> 2) & 1));   // the team's partials and y_k
-                mbar_wait(pbar + k % C::kPbuf, (uint32_t)((k / C::kPbuf) & 1));   // the lieutenants' q_l
+                // y_k - sum_l q_l (the lieutenants' D_k^{-1}-multiplied partials), overlapping the
+                // other warps' partials
+                mbar_wait(pbar + k % C::kPbuf, (uint32_t)((k / C::kPbuf) & 1));
+#pragma unroll
+                for (int l = 0; l < C::kLt; l++) yk = csub(yk, pbuf[((k % C::kPbuf) * C::kLt + l) * B + lane]);
+                mbar_wait(pready + pq, (uint32_t)((k >> 2) & 1));   // the team's partials
                 TPROF(k, 4);
                 if (trace && tw == 0 && lane == 0) STAMP(k, 0);
                 double2 sum = tpart[(pq * C::kTeam + 0) * B + lane];
 #pragma unroll
                 for (int w = 1; w < C::kTeam; w++) sum = cadd(sum, tpart[(pq * C::kTeam + w) * B + lane]);
-#pragma unroll
-                for (int l = 0; l < C::kLt; l++) sum = cadd(sum, pbuf[((k % C::kPbuf) * C::kLt + l) * B + lane]);
                 const double2 xk = csub(yk, sum);
                 TPROF(k, 5);
                 if (tw == 0) {
@@ -594,7 +634,9 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                 for (int k = lteam; k < nblk; k += C::kLtTeams) {
                     const int s = k % nst;
                     unsigned char* st = smem + stsz * s;
+                    LPROF(k, 0);
                     mbar_wait(full + s, (uint32_t)((k / nst) & 1));
+                    LPROF(k, 1);
                     const bool tr0 = trace && tt == 0 && l == 0;
                     if (tr0) STAMP(k, 12);
                     const int32_t* loc = reinterpret_cast<const int32_t*>(st + C::kOffBloc);
@@ -602,41 +644,55 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     const double2* val = reinterpret_cast<const double2*>(st + C::kOffBval);
                     double2 acc = make_double2(0.0, 0.0);
                     land(k - kDense - 2);
+                    LPROF(k, 2);
                     if (rowok) acc = near_range<B, C::kTPRl, C::kRingLt>(col, val, ltring, loc[r], loc[C::kLate + r], q, acc);
-                    if (tr0) STAMP(k, 11);
-                    land(k - kDense - 1);
-                    if (tr0) STAMP(k, 7);
-                    if (rowok) acc = near_range<B, C::kTPRl, C::kRingLt>(col, val, ltring, loc[C::kLate + r], loc[r + 1], q, acc);
 #pragma unroll
-                    for (int o = 1; o < C::kTPRl; o <<= 1) {
+                    for (int o = 1; o < C::kTPRl; o <<= 1) {   // the early part, reduced before the late one lands
                         acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
                         acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
                     }
+                    if (q != 0) acc = make_double2(0.0, 0.0);
+                    const int lt0 = rowok ? loc[C::kLate + r] : 0, lt1 = rowok ? loc[r + 1] : 0;   // late part
+                    LPROF(k, 3);
+                    if (tr0) STAMP(k, 11);
+                    land(k - kDense - 1);
+                    LPROF(k, 4);
+                    if (tr0) STAMP(k, 7);
+                    // the late part (a few entries per row): the row's first thread alone
+                    if (rowok && q == 0) acc = row_sum_1t<B, C::kRingLt>(col, val, ltring, lt0, lt1, acc);
+                    LPROF(k, 5);
                     if (rowok && q == 0) lp[r] = acc;
                     bar_named(2 + lteam, C::kLtTeamT);
-                    // q_l = D_k^{-1}[:, rows of l] p_l: output row i = tt / 4, the rows m = part,
-                    // part + 4, ... of this lieutenant (4 threads per output row)
-                    {
+                    LPROF(k, 6);
+                    // q_l = D_k^{-1}[:, rows of l] p_l: one thread per output row i (the team's first
+                    // warp), the lieutenant's rows rr = l, l + kLt, ... <= i in order
+                    if (tt < B) {
                         const double2* sInv = reinterpret_cast<const double2*>(st + C::kOffBinv);
-                        const int i = tt >> 2, part = tt & 3;
-                        double2 qa = make_double2(0.0, 0.0);
+                        const int i = tt;
+                        double2 qa = make_double2(0.0, 0.0), qb = make_double2(0.0, 0.0);
+                        constexpr int kRows = (B + C::kLt - 1) / C::kLt;
+                        double2 dq[kRows], pq[kRows];
 #pragma unroll
-                        for (int m = part; m * C::kLt + l < B; m += 4) {
+                        for (int m = 0; m < kRows; m++) {   // predicated loads: D^{-1}[i, rr] is 0 above the diagonal
                             const int rr = m * C::kLt + l;
-                            if (rr <= i) qa = cfma(qa, sInv[rr * B - (rr * (rr - 1)) / 2 + (i - rr)], lp[rr]);
+                            const bool ok = rr <= i;
+                            dq[m] = sInv[ok ? rr * B - (rr * (rr - 1)) / 2 + (i - rr) : 0];
+                            dq[m].x = ok ? dq[m].x : 0.0;
+                            dq[m].y = ok ? dq[m].y : 0.0;
+                            pq[m] = lp[rr < B ? rr : 0];
                         }
 #pragma unroll
-                        for (int o = 1; o < 4; o <<= 1) {
-                            qa.x += __shfl_xor_sync(0xffffffffu, qa.x, o);
-                            qa.y += __shfl_xor_sync(0xffffffffu, qa.y, o);
+                        for (int m = 0; m < kRows; m += 2) {
+                            qa = cfma(qa, dq[m], pq[m]);
+                            if (m + 1 < kRows) qb = cfma(qb, dq[m + 1], pq[m + 1]);
                         }
-                        if (part == 0) {
-                            const int pk = k % C::kPbuf;
-                            st_async2(peer_pbuf + (uint32_t)(((pk * C::kLt + l) * B + i) * 16), qa,
-                                      peer_pbar + (uint32_t)(pk * 8));
-                        }
+                        const int pk = k % C::kPbuf;
+                        st_async2(peer_pbuf + (uint32_t)(((pk * C::kLt + l) * B + i) * 16), cadd(qa, qb),
+                                  peer_pbar + (uint32_t)(pk * 8));
+                        LPROF(k, 7);
                     }
                     bar_named(2 + lteam, C::kLtTeamT);
+                    LPROF(k, 8);
                     if (tt == 0) {
                         mbar_arrive(empty + s);
 
