@@ -50,7 +50,7 @@ struct HostCSR {
 //   d = 1 .. kDense  -> dense G_d = D_k^{-1} T_{k,k-d} (the chain teams)
 //   kDense < d < Q_k -> list B, staged per lieutenant CTA and block
 //   d >= Q_k         -> far part (helper CTAs)
-constexpr int kDense = 3;
+constexpr int kDense = 2;
 constexpr int near_cap_b(int B) { return B <= 32 ? 1024 : 1024; }   // per lieutenant and block
 constexpr int kLieutenants = 7;   // list B CTAs of a chain cluster (trsv.cu; cluster = 1 + 7)
 constexpr int near_nloc(int B) { return 2 * (B + 4); }   // per list: row starts | late-part starts

@@ -241,7 +241,7 @@ struct Cfg {
     static constexpr size_t kOffRfull = kOffPready + 8 * 4;
     static constexpr size_t kOffInts = kOffRfull + 8 * kSStages;
     static constexpr size_t kSmem = kOffInts + 64;
-    static_assert(B == 32 && kDense == 3, "the chain teams hold one row per lane and the G1, G2, G3 blocks");
+    static_assert(B == 32 && (kDense == 2 || kDense == 3), "the chain teams hold one row per lane, G1 .. G_kDense");
     static_assert(kCompute % B == 0 && B % kFarWarps == 0 && kRPW % kGrp == 0, "layout");
     static_assert(kTeamW0 + kTeams * kTeam == kNT / 32 && kCompute / 32 + 1 <= kNT / 32, "warp roles");
     static_assert(kTPRl * ((B + kLt - 1) / kLt) <= kLtTeamT && kLtTeams * kLtTeamT <= 32 * kWProducerLt &&
@@ -520,10 +520,12 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     for (int u = 0; u < C::kSlice; u++) g1[u] = G[(j0 + u) * B + lane];
                     TPROF(k, 10);
                     double2 c1 = make_double2(0.0, 0.0);
-                    if (k >= 3) {   // x_{k-3}: this team's previous block
+                    if constexpr (kDense >= 3) {
+                        if (k >= 3) {   // x_{k-3}: this team's previous block
 #pragma unroll
-                        for (int u = 0; u < C::kSlice; u++)
-                            c1 = cfma(c1, G[2 * B * B + (j0 + u) * B + lane], xw[j0 + u]);
+                            for (int u = 0; u < C::kSlice; u++)
+                                c1 = cfma(c1, G[2 * B * B + (j0 + u) * B + lane], xw[j0 + u]);
+                        }
                     }
                     TPROF(k, 11);
                     if (k >= 2) {
@@ -578,6 +580,7 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                 // y_k - sum_l q_l (the lieutenants' D_k^{-1}-multiplied partials), overlapping the
                 // other warps' partials
                 mbar_wait(pbar + k % C::kPbuf, (uint32_t)((k / C::kPbuf) & 1));
+                if (trace && tw == 0 && lane == 0) STAMP(k, 6);
 #pragma unroll
                 for (int l = 0; l < C::kLt; l++) yk = csub(yk, pbuf[((k % C::kPbuf) * C::kLt + l) * B + lane]);
                 mbar_wait(pready + pq, (uint32_t)((k >> 2) & 1));   // the team's partials
@@ -690,6 +693,8 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                         st_async2(peer_pbuf + (uint32_t)(((pk * C::kLt + l) * B + i) * 16), cadd(qa, qb),
                                   peer_pbar + (uint32_t)(pk * 8));
                         LPROF(k, 7);
+                        if (tr0) STAMP(k, 9);
+                        if (trace && tt == 0 && l == C::kLt - 1) STAMP(k, 2);
                     }
                     bar_named(2 + lteam, C::kLtTeamT);
                     LPROF(k, 8);
