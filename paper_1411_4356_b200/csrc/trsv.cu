@@ -388,8 +388,8 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
         }
         for (int j = 0; j < C::kRingLt; j++) mbar_init(xbar + j, 1);
         for (int j = 0; j < C::kPbuf; j++) mbar_init(pbar + j, 1);
-        for (int j = 0; j < C::kRing; j++) mbar_init(xfull + j, 1);
-        for (int j = 0; j < 4; j++) mbar_init(pready + j, C::kTeam);
+        for (int j = 0; j < C::kRing; j++) mbar_init(xfull + j, 32);   // the 32 lanes of the storing warp
+        for (int j = 0; j < 4; j++) mbar_init(pready + j, C::kTeam * 32);   // every lane of a team
         *sDone = 0;
         *sF = 0;
         *sLock = 0;
@@ -568,14 +568,16 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                 TPROF(k, 2);
                 if (trace && tw == 0 && lane == 0) STAMP(k, 13);
                 double2 p0 = carry, p1 = make_double2(0.0, 0.0);
+                double2 p2 = make_double2(0.0, 0.0), p3 = make_double2(0.0, 0.0);
 #pragma unroll
-                for (int u = 0; u < C::kSlice; u += 2) {
+                for (int u = 0; u < C::kSlice; u += 4) {
                     p0 = cfma(p0, g1[u], xs[u]);
                     p1 = cfma(p1, g1[u + 1], xs[u + 1]);
+                    p2 = cfma(p2, g1[u + 2], xs[u + 2]);
+                    p3 = cfma(p3, g1[u + 3], xs[u + 3]);
                 }
-                tpart[(pq * C::kTeam + tw) * B + lane] = cadd(p0, p1);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(pready + pq);   // this warp's partial is in tpart
+                tpart[(pq * C::kTeam + tw) * B + lane] = cadd(cadd(p0, p1), cadd(p2, p3));
+                mbar_arrive(pready + pq);   // every lane, after its own partial
                 TPROF(k, 3);
                 // y_k - sum_l q_l (the lieutenants' D_k^{-1}-multiplied partials), overlapping the
                 // other warps' partials
@@ -593,8 +595,7 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                 TPROF(k, 5);
                 if (tw == 0) {
                     ring[((int64_t)k * B + lane) & kRingMask] = xk;
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(xfull + k % C::kRing);   // release: x_k is in the ring
+                    mbar_arrive(xfull + k % C::kRing);   // every lane releases its own x_k[lane]
                     TPROF(k, 6);
                     if (trace && lane == 0) STAMP(k, 3);
                 } else if (tw == 1) {
@@ -662,7 +663,24 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     LPROF(k, 4);
                     if (tr0) STAMP(k, 7);
                     // the late part (a few entries per row): the row's first thread alone
-                    if (rowok && q == 0) acc = row_sum_1t<B, C::kRingLt>(col, val, ltring, lt0, lt1, acc);
+                    if (rowok && q < C::kTPRlate) {   // entries lt0 + q, lt0 + q + kTPRlate, ... (predicated)
+                        constexpr int kRM = C::kRingLt * B - 1;
+                        for (int e = lt0 + q; e < lt1; e += 2 * C::kTPRlate) {
+                            const bool ok = e + C::kTPRlate < lt1;
+                            const int e1 = ok ? e + C::kTPRlate : e;
+                            const int c0 = col[e], c1 = col[e1];
+                            double2 v1 = val[e1];
+                            v1.x = ok ? v1.x : 0.0;
+                            v1.y = ok ? v1.y : 0.0;
+                            acc = cfma(acc, val[e], ltring[c0 & kRM]);
+                            acc = cfma(acc, v1, ltring[c1 & kRM]);
+                        }
+                    }
+#pragma unroll
+                    for (int o = 1; o < C::kTPRlate; o <<= 1) {
+                        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+                        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+                    }
                     LPROF(k, 5);
                     if (rowok && q == 0) lp[r] = acc;
                     bar_named(2 + lteam, C::kLtTeamT);
@@ -721,9 +739,15 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
     int64_t* sRowP = reinterpret_cast<int64_t*>(smem + C::kOffRowP);
     int32_t* sRowL = reinterpret_cast<int32_t*>(smem + C::kOffRowL);
     double2* sRf = reinterpret_cast<double2*>(smem + C::kOffR);   // b_k - far part
+    const double2* hInv = reinterpret_cast<const double2*>(smem);  // D_k^{-1}, staged by TMA
     const int yi = tid >> 3, yp = tid & 7;                         // D^{-1} product: row, column class
-    for (int k = blockIdx.x - C::kCluster; k < nblk; k += H) {
+    int hit = 0;                                                   // blocks done by this CTA
+    for (int k = blockIdx.x - C::kCluster; k < nblk; k += H, hit++) {
         const int64_t row0 = (int64_t)k * B;
+        if (tid == 0) {   // D_k^{-1} lands while the far part streams (full[0]: this CTA's barrier)
+            mbar_expect_tx(full, (uint32_t)(C::kPK * 16));
+            bulk_g2s(smem, a.dinv + (int64_t)k * C::kPK, C::kPK * 16, full);
+        }
         double2 acc[C::kRPW];
         int64_t* wp = sRowP + warp * C::kRPW;
         int32_t* wl = sRowL + warp * C::kRPW;
@@ -781,14 +805,14 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
             const int64_t i = row0 + warp * C::kRPW + r;
             if (lane == 0) sRf[warp * C::kRPW + r] = (i < n) ? csub(__ldg(bvec + phys(i)), sm) : make_double2(0.0, 0.0);
         }
+        bar_named(1, C::kCompute);
+        mbar_wait(full, (uint32_t)(hit & 1));
         double2 dv[B / 8];   // D_k^{-1}[yi, yp + 8m]
 #pragma unroll
         for (int m = 0; m < B / 8; m++) {
             const int j = yp + 8 * m;
-            dv[m] = j <= yi ? __ldg(a.dinv + (int64_t)k * C::kPK + j * B - (j * (j - 1)) / 2 + (yi - j))
-                            : make_double2(0.0, 0.0);
+            dv[m] = j <= yi ? hInv[j * B - (j * (j - 1)) / 2 + (yi - j)] : make_double2(0.0, 0.0);
         }
-        bar_named(1, C::kCompute);
         // y_k = D_k^{-1} (b_k - far part): output row yi = tid / 8, columns j = yp, yp + 8, ...
         {
             double2 ya = make_double2(0.0, 0.0);
