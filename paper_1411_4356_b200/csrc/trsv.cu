@@ -184,7 +184,7 @@ struct Cfg {
     static constexpr int kTeam = 4, kTeams = 3, kTeamW0 = 5;
     static constexpr int kWProducerChain = 0, kWPublisher = 1, kWGProducer = 2;
     static constexpr int kSlice = B / kTeam;          // columns of G per team warp
-    static constexpr int kFarWarps = kCompute / 32;   // helper warps streaming the far part
+    static constexpr int kFarWarps = 16;              // helper warps streaming the far part
     static constexpr int kRPW = B / kFarWarps;        // far rows per helper warp
     static constexpr int kGrp = kRPW < 4 ? kRPW : 4;
     static constexpr int kGStages = 3;                // G1 | G2 | G3 ring (chain teams, a block ahead)
@@ -242,7 +242,9 @@ struct Cfg {
     static constexpr size_t kOffInts = kOffRfull + 8 * kSStages;
     static constexpr size_t kSmem = kOffInts + 64;
     static_assert(B == 32 && (kDense == 2 || kDense == 3), "the chain teams hold one row per lane, G1 .. G_kDense");
-    static_assert(kCompute % B == 0 && B % kFarWarps == 0 && kRPW % kGrp == 0, "layout");
+    static_assert(kCompute % B == 0 && B % kFarWarps == 0 && kRPW % kGrp == 0 && kFarWarps * 32 <= kNT, "layout");
+    static constexpr int kHelperT = kFarWarps * 32;   // helper threads
+    static constexpr int kYP = kHelperT / B;          // helper D^{-1} product: threads per row
     static_assert(kTeamW0 + kTeams * kTeam == kNT / 32 && kCompute / 32 + 1 <= kNT / 32, "warp roles");
     static_assert(kTPRl * ((B + kLt - 1) / kLt) <= kLtTeamT && kLtTeams * kLtTeamT <= 32 * kWProducerLt &&
                       kLtTeams <= kLtStages,
@@ -404,38 +406,54 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
         unsigned char* const sbase = smem + (chain ? C::kOffSR : 0);
         const int wprod = chain ? C::kWProducerChain : C::kWProducerLt;
         if (warp == wprod) {
-            // ------------------------------------------------ producer: TMA staging; lane 0 the
-            // S ring (lieutenants: list B), lane 1 the chain's G ring (independent of the helpers)
-            if (lane == 0) {
+            // ------------------------------------------------ producer: TMA staging of the S ring
+            // (chain: y_k once its helper flag is set, the 32 lanes polling 32 flags per round
+            // trip; lieutenants: list B and D_k^{-1})
+            if (chain) {
+                int k = 0;
+                while (k < nblk) {
+                    const int kk = k + lane;
+                    const bool ready = kk < nblk && ld_acquire(a.fflag + kk) == epoch;
+                    const unsigned m = __ballot_sync(0xffffffffu, ready);
+                    const int nready = m == 0xffffffffu ? 32 : __ffs(~m) - 1;   // consecutive from k
+                    if (nready == 0) {
+                        __nanosleep(kProducerSleep);
+                        continue;
+                    }
+                    if (lane == 0) {
+                        fence_proxy_async();   // y (generic-proxy stores of the helpers) -> TMA reads
+                        for (int j = k; j < k + nready && j < nblk; j++) {
+                            const int s = j % nst;
+                            if (j >= nst) mbar_wait(empty + s, (uint32_t)((j / nst - 1) & 1));
+                            if (trace) STAMP(j, 5);
+                            mbar_expect_tx(rfull + s, (uint32_t)(B * 16));
+                            bulk_g2s(sbase + stsz * s, a.yfar + (int64_t)j * B, B * 16, rfull + s);
+                        }
+                    }
+                    __syncwarp();
+                    k += nready;
+                }
+            } else if (lane == 0) {
                 // lieutenants: the list bounds of block k+1 are loaded while block k's slot drains
                 int64_t nb0 = 0, nb1 = 0;
-                if (!chain && nblk > 0) {
+                if (nblk > 0) {
                     nb0 = __ldg(a.nbpB + (role - 1));
                     nb1 = __ldg(a.nbpB + role);
                 }
                 for (int k = 0; k < nblk; k++) {
                     const int s = k % nst;
                     const int64_t b0 = nb0, b1 = nb1;
-                    if (!chain && k + 1 < nblk) {
+                    if (k + 1 < nblk) {
                         const int gn = (k + 1) * C::kLt + (role - 1);
                         nb0 = __ldg(a.nbpB + gn);
                         nb1 = __ldg(a.nbpB + gn + 1);
                     }
                     if (k >= nst) mbar_wait(empty + s, (uint32_t)((k / nst - 1) & 1));
                     unsigned char* st = sbase + stsz * s;
-                    if (chain) {
-                        // y_k once the helpers have published it
-                        while (ld_acquire(a.fflag + k) != epoch) __nanosleep(kProducerSleep);
-                        if (trace) STAMP(k, 5);
-                        fence_proxy_async();   // y_k (generic-proxy stores of a helper) -> TMA reads
-                        mbar_expect_tx(rfull + s, (uint32_t)(B * 16));
-                        bulk_g2s(st, a.yfar + (int64_t)k * B, B * 16, rfull + s);
-                    } else {
-                        const int g = k * C::kLt + (role - 1);   // this lieutenant's rows of block k
-                        stage_near(st + C::kOffBcol, st + C::kOffBval, st + C::kOffBloc, b0, b1, a.ncolB, a.nvalB,
-                                   a.nlocB, g, C::kNloc, full + s, (uint32_t)(C::kPK * 16));
-                        bulk_g2s(st + C::kOffBinv, a.dinv + (int64_t)k * C::kPK, C::kPK * 16, full + s);
-                    }
+                    const int g = k * C::kLt + (role - 1);   // this lieutenant's rows of block k
+                    stage_near(st + C::kOffBcol, st + C::kOffBval, st + C::kOffBloc, b0, b1, a.ncolB, a.nvalB,
+                               a.nlocB, g, C::kNloc, full + s, (uint32_t)(C::kPK * 16));
+                    bulk_g2s(st + C::kOffBinv, a.dinv + (int64_t)k * C::kPK, C::kPK * 16, full + s);
                 }
             }
         } else if (chain && warp == C::kWGProducer) {
@@ -740,7 +758,7 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
     int32_t* sRowL = reinterpret_cast<int32_t*>(smem + C::kOffRowL);
     double2* sRf = reinterpret_cast<double2*>(smem + C::kOffR);   // b_k - far part
     const double2* hInv = reinterpret_cast<const double2*>(smem);  // D_k^{-1}, staged by TMA
-    const int yi = tid >> 3, yp = tid & 7;                         // D^{-1} product: row, column class
+    const int yi = tid / C::kYP, yp = tid % C::kYP;               // D^{-1} product: row, column class
     int hit = 0;                                                   // blocks done by this CTA
     for (int k = blockIdx.x - C::kCluster; k < nblk; k += H, hit++) {
         const int64_t row0 = (int64_t)k * B;
@@ -805,28 +823,28 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
             const int64_t i = row0 + warp * C::kRPW + r;
             if (lane == 0) sRf[warp * C::kRPW + r] = (i < n) ? csub(__ldg(bvec + phys(i)), sm) : make_double2(0.0, 0.0);
         }
-        bar_named(1, C::kCompute);
+        bar_named(1, C::kHelperT);
         mbar_wait(full, (uint32_t)(hit & 1));
-        double2 dv[B / 8];   // D_k^{-1}[yi, yp + 8m]
+        double2 dv[B / C::kYP];   // D_k^{-1}[yi, yp + kYP m]
 #pragma unroll
-        for (int m = 0; m < B / 8; m++) {
-            const int j = yp + 8 * m;
+        for (int m = 0; m < B / C::kYP; m++) {
+            const int j = yp + C::kYP * m;
             dv[m] = j <= yi ? hInv[j * B - (j * (j - 1)) / 2 + (yi - j)] : make_double2(0.0, 0.0);
         }
-        // y_k = D_k^{-1} (b_k - far part): output row yi = tid / 8, columns j = yp, yp + 8, ...
+        // y_k = D_k^{-1} (b_k - far part): output row yi, columns j = yp, yp + kYP, ...
         {
             double2 ya = make_double2(0.0, 0.0);
 #pragma unroll
-            for (int m = 0; m < B / 8; m++)
-                if (yp + 8 * m <= yi) ya = cfma(ya, dv[m], sRf[yp + 8 * m]);
+            for (int m = 0; m < B / C::kYP; m++)
+                if (yp + C::kYP * m <= yi) ya = cfma(ya, dv[m], sRf[yp + C::kYP * m]);
 #pragma unroll
-            for (int o = 1; o < 8; o <<= 1) {
+            for (int o = 1; o < C::kYP; o <<= 1) {
                 ya.x += __shfl_xor_sync(0xffffffffu, ya.x, o);
                 ya.y += __shfl_xor_sync(0xffffffffu, ya.y, o);
             }
             if (yp == 0) a.yfar[row0 + yi] = ya;
         }
-        bar_named(1, C::kCompute);
+        bar_named(1, C::kHelperT);
         if (tid == 0) {
             st_release(a.fflag + k, epoch);
             if (trace) STAMP(k, 4);
