@@ -675,24 +675,47 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     }
                     if (q != 0) acc = make_double2(0.0, 0.0);
                     const int lt0 = rowok ? loc[C::kLate + r] : 0, lt1 = rowok ? loc[r + 1] : 0;   // late part
+                    // the late part's first 2 kTPRlate entries of the row: columns and values now,
+                    // x once it has landed (predicated: absent entries get value 0)
+                    constexpr int kRM = C::kRingLt * B - 1;
+                    int lc0 = 0, lc1 = 0;
+                    double2 lv0 = make_double2(0.0, 0.0), lv1 = make_double2(0.0, 0.0);
+                    if (rowok && q < C::kTPRlate) {
+                        const int e0 = lt0 + q, e1 = e0 + C::kTPRlate;
+                        const bool ok0 = e0 < lt1, ok1 = e1 < lt1;
+                        lc0 = col[ok0 ? e0 : 0];
+                        lc1 = col[ok1 ? e1 : 0];
+                        lv0 = val[ok0 ? e0 : 0];
+                        lv1 = val[ok1 ? e1 : 0];
+                        lv0.x = ok0 ? lv0.x : 0.0;
+                        lv0.y = ok0 ? lv0.y : 0.0;
+                        lv1.x = ok1 ? lv1.x : 0.0;
+                        lv1.y = ok1 ? lv1.y : 0.0;
+                    }
+                    // and this thread's entries of D_k^{-1} for the q product below
+                    constexpr int kRows = (B + C::kLt - 1) / C::kLt;
+                    double2 dq[kRows];
+                    if (tt < B) {
+                        const double2* sInv = reinterpret_cast<const double2*>(st + C::kOffBinv);
+#pragma unroll
+                        for (int m = 0; m < kRows; m++) {   // predicated loads: D^{-1}[i, rr] is 0 above the diagonal
+                            const int rr = m * C::kLt + l;
+                            const bool ok = rr <= tt;
+                            dq[m] = sInv[ok ? rr * B - (rr * (rr - 1)) / 2 + (tt - rr) : 0];
+                            dq[m].x = ok ? dq[m].x : 0.0;
+                            dq[m].y = ok ? dq[m].y : 0.0;
+                        }
+                    }
                     LPROF(k, 3);
                     if (tr0) STAMP(k, 11);
                     land(k - kDense - 1);
                     LPROF(k, 4);
                     if (tr0) STAMP(k, 7);
-                    // the late part (a few entries per row): the row's first thread alone
-                    if (rowok && q < C::kTPRlate) {   // entries lt0 + q, lt0 + q + kTPRlate, ... (predicated)
-                        constexpr int kRM = C::kRingLt * B - 1;
-                        for (int e = lt0 + q; e < lt1; e += 2 * C::kTPRlate) {
-                            const bool ok = e + C::kTPRlate < lt1;
-                            const int e1 = ok ? e + C::kTPRlate : e;
-                            const int c0 = col[e], c1 = col[e1];
-                            double2 v1 = val[e1];
-                            v1.x = ok ? v1.x : 0.0;
-                            v1.y = ok ? v1.y : 0.0;
-                            acc = cfma(acc, val[e], ltring[c0 & kRM]);
-                            acc = cfma(acc, v1, ltring[c1 & kRM]);
-                        }
+                    if (rowok && q < C::kTPRlate) {
+                        acc = cfma(acc, lv0, ltring[lc0 & kRM]);
+                        acc = cfma(acc, lv1, ltring[lc1 & kRM]);
+                        for (int e = lt0 + q + 2 * C::kTPRlate; e < lt1; e += C::kTPRlate)   // long rows
+                            acc = cfma(acc, val[e], ltring[col[e] & kRM]);
                     }
 #pragma unroll
                     for (int o = 1; o < C::kTPRlate; o <<= 1) {
@@ -706,18 +729,12 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     // q_l = D_k^{-1}[:, rows of l] p_l: one thread per output row i (the team's first
                     // warp), the lieutenant's rows rr = l, l + kLt, ... <= i in order
                     if (tt < B) {
-                        const double2* sInv = reinterpret_cast<const double2*>(st + C::kOffBinv);
                         const int i = tt;
                         double2 qa = make_double2(0.0, 0.0), qb = make_double2(0.0, 0.0);
-                        constexpr int kRows = (B + C::kLt - 1) / C::kLt;
-                        double2 dq[kRows], pq[kRows];
+                        double2 pq[kRows];
 #pragma unroll
-                        for (int m = 0; m < kRows; m++) {   // predicated loads: D^{-1}[i, rr] is 0 above the diagonal
+                        for (int m = 0; m < kRows; m++) {
                             const int rr = m * C::kLt + l;
-                            const bool ok = rr <= i;
-                            dq[m] = sInv[ok ? rr * B - (rr * (rr - 1)) / 2 + (i - rr) : 0];
-                            dq[m].x = ok ? dq[m].x : 0.0;
-                            dq[m].y = ok ? dq[m].y : 0.0;
                             pq[m] = lp[rr < B ? rr : 0];
                         }
 #pragma unroll
