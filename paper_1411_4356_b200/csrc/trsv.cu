@@ -16,22 +16,22 @@
 // kernel's index space (U reversed at setup, i' = n-1-i, so both factors are lower
 // triangular)
 //     x_k = D_k^{-1} ( b_k - sum_{j<k} T_kj x_j )
-//         = y_k - sum_l q_{l,k} - G1_k x_{k-1} - G2_k x_{k-2} - G3_k x_{k-3},
+//         = y_k - sum_l q_{l,k} - G1_k x_{k-1} - G2_k x_{k-2}        (kDense = 2),
 //     y_k = D_k^{-1} ( b_k - far_k ),  Gd_k = D_k^{-1} T_{k,k-d} (dense, precomputed),
 //     q_{l,k} = D_k^{-1}[:, rows of l] (list B of lieutenant l applied to x),
 // where "far" are the entries with source distance d >= Q_k and list B those with
-// 4 <= d < Q_k (setup.cpp::build_block_tri).  Only G1_k x_{k-1} is on the chain:
+// kDense < d < Q_k (setup.cpp::build_block_tri).  Only G1_k x_{k-1} is on the chain:
 //   * chain CTA (cluster rank 0): three chain teams of 4 warps rotate over the blocks;
-//     the team of block k prepares G1_k (registers), the carry G2_k x_{k-2} + G3_k x_{k-3}
-//     and y_k - sum_l q_l while the other teams compute x_{k-2}, x_{k-1}; then x_{k-1}
+//     the team of block k prepares G1_k (registers), the carry G2_k x_{k-2} and y_k while
+//     the other teams compute x_{k-2}, x_{k-1}; then x_{k-1}
 //     (ring + mbarrier) -> G1_k x_{k-1} -> partials (mbarrier) -> x_k into the ring and,
 //     by st.async, into the lieutenants' rings;
 //   * lieutenants (cluster ranks 1..7, DSMEM): list B of rows l, l+7, ..., the early
-//     part (d >= 5) once x_{k-5} has landed, the late part (d = 4) once x_{k-4} has, times
+//     part (d >= 4) once x_{k-4} has landed, the late part (d = 3) once x_{k-3} has, times
 //     their columns of D_k^{-1}, st.async'd back to the chain CTA;
 //   * helpers (the other SMs): the far entries streamed in 32-entry chunks as the
 //     published frontier covers them; y_k published with a gpu-scope release flag;
-//   * producer warps: TMA bulk copies (cp.async.bulk + mbarrier) of G1|G2|G3 and y_k
+//   * producer warps: TMA bulk copies (cp.async.bulk + mbarrier) of G1|G2 and y_k
 //     (chain CTA) or list B and D_k^{-1} (lieutenants), stages ahead;
 //   * publisher warp: copies finished x blocks from the ring to global memory (and
 //     through the iLUTP column permutation to the output, x = Pi y) and advances the
