@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--workload", default="small", choices=["tiny", "small", "medium", "large"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--threads", type=int, default=0, help="host threads for the ILUT setup")
-    ap.add_argument("--dims", default="tiny,small",
+    ap.add_argument("--dims", default="tiny,small,medium",
                     help="configs for the time-to-steady-state vs Liouvillian-dim table (rank 0, N = 1)")
     return ap.parse_args()
 

@@ -211,9 +211,10 @@ struct Cfg {
     static constexpr size_t kOffBcol = 0;
     static constexpr size_t kOffBval = kOffBcol + (size_t)kCapB * 4;
     static constexpr size_t kOffBloc = kOffBval + (size_t)kCapB * 16;
-    static constexpr size_t kOffBinv = kOffBloc + (size_t)kNloc * 4;   // D_k^{-1} (packed)
-    static constexpr size_t kLtStage = kOffBinv + (size_t)kPK * 16;
-    static constexpr int kLtStages = 6;
+    static constexpr int kRowsL = lt_rows(B);         // rows of a block per lieutenant
+    static constexpr size_t kOffBinv = kOffBloc + (size_t)kNloc * 4;   // this lieutenant's columns of D_k^{-1}
+    static constexpr size_t kLtStage = kOffBinv + (size_t)kRowsL * B * 16;
+    static constexpr int kLtStages = 7;
     static constexpr size_t kOffLtRing = kLtStage * kLtStages;   // lieutenants' x ring
     static constexpr size_t kOffLtP = kOffLtRing + (size_t)kRingLt * B * 16;   // [kLtTeams][B] row partials
     static constexpr size_t kLtRegion = kOffLtP + (size_t)kLtTeams * B * 16;
@@ -452,8 +453,8 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     unsigned char* st = sbase + stsz * s;
                     const int g = k * C::kLt + (role - 1);   // this lieutenant's rows of block k
                     stage_near(st + C::kOffBcol, st + C::kOffBval, st + C::kOffBloc, b0, b1, a.ncolB, a.nvalB,
-                               a.nlocB, g, C::kNloc, full + s, (uint32_t)(C::kPK * 16));
-                    bulk_g2s(st + C::kOffBinv, a.dinv + (int64_t)k * C::kPK, C::kPK * 16, full + s);
+                               a.nlocB, g, C::kNloc, full + s, (uint32_t)(C::kRowsL * B * 16));
+                    bulk_g2s(st + C::kOffBinv, a.dinvl + (int64_t)g * C::kRowsL * B, C::kRowsL * B * 16, full + s);
                 }
             }
         } else if (chain && warp == C::kWGProducer) {
@@ -635,7 +636,8 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
             // ------------------------------------------------ lieutenants: list B partial sums
             // (source distance kDense+1 .. Q_k-1) of the rows l, l+kLt, ...; kLtTeams teams of
             // 4 warps take the blocks k mod kLtTeams.  The early part (distance >= kDense+2) is
-            // summed before x_{k-kDense-1} lands, the late part after.  x blocks land by
+            // summed once x_{k-kDense-2} has landed, the late part (kDense+1) once x_{k-kDense-1}
+            // has.  x blocks land by
             // st.async from the chain team, which also makes each xbar phase's one arrival.
             // Each lieutenant sends q_l = D_k^{-1}[:, its rows] (its row partials), so the chain
             // only subtracts the three q_l from y_k = D_k^{-1} r_k.
@@ -675,36 +677,31 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     }
                     if (q != 0) acc = make_double2(0.0, 0.0);
                     const int lt0 = rowok ? loc[C::kLate + r] : 0, lt1 = rowok ? loc[r + 1] : 0;   // late part
-                    // the late part's first 2 kTPRlate entries of the row: columns and values now,
+                    // the first 2 kTPRlate entries of the row's late part: columns and values now,
                     // x once it has landed (predicated: absent entries get value 0)
                     constexpr int kRM = C::kRingLt * B - 1;
                     int lc0 = 0, lc1 = 0;
-                    double2 lv0 = make_double2(0.0, 0.0), lv1 = make_double2(0.0, 0.0);
-                    if (rowok && q < C::kTPRlate) {
-                        const int e0 = lt0 + q, e1 = e0 + C::kTPRlate;
-                        const bool ok0 = e0 < lt1, ok1 = e1 < lt1;
-                        lc0 = col[ok0 ? e0 : 0];
-                        lc1 = col[ok1 ? e1 : 0];
-                        lv0 = val[ok0 ? e0 : 0];
-                        lv1 = val[ok1 ? e1 : 0];
-                        lv0.x = ok0 ? lv0.x : 0.0;
-                        lv0.y = ok0 ? lv0.y : 0.0;
-                        lv1.x = ok1 ? lv1.x : 0.0;
-                        lv1.y = ok1 ? lv1.y : 0.0;
-                    }
+                    double2 lv0 = make_double2(0.0, 0.0), lv1 = lv0;
+                    auto pre = [&](int p0, int p1, int& c0, int& c1, double2& v0, double2& v1) {
+                        const int e0 = p0 + q, e1 = e0 + C::kTPRlate;
+                        const bool ok0 = e0 < p1, ok1 = e1 < p1;
+                        c0 = col[ok0 ? e0 : 0];
+                        c1 = col[ok1 ? e1 : 0];
+                        v0 = val[ok0 ? e0 : 0];
+                        v1 = val[ok1 ? e1 : 0];
+                        v0.x = ok0 ? v0.x : 0.0;
+                        v0.y = ok0 ? v0.y : 0.0;
+                        v1.x = ok1 ? v1.x : 0.0;
+                        v1.y = ok1 ? v1.y : 0.0;
+                    };
+                    if (rowok && q < C::kTPRlate) pre(lt0, lt1, lc0, lc1, lv0, lv1);
                     // and this thread's entries of D_k^{-1} for the q product below
-                    constexpr int kRows = (B + C::kLt - 1) / C::kLt;
-                    double2 dq[kRows];
+                    constexpr int kRows = C::kRowsL;
+                    double2 dq[kRows];   // D_k^{-1}[tt, l + kLt m] (staged zero above the diagonal)
                     if (tt < B) {
                         const double2* sInv = reinterpret_cast<const double2*>(st + C::kOffBinv);
 #pragma unroll
-                        for (int m = 0; m < kRows; m++) {   // predicated loads: D^{-1}[i, rr] is 0 above the diagonal
-                            const int rr = m * C::kLt + l;
-                            const bool ok = rr <= tt;
-                            dq[m] = sInv[ok ? rr * B - (rr * (rr - 1)) / 2 + (tt - rr) : 0];
-                            dq[m].x = ok ? dq[m].x : 0.0;
-                            dq[m].y = ok ? dq[m].y : 0.0;
-                        }
+                        for (int m = 0; m < kRows; m++) dq[m] = sInv[m * B + tt];
                     }
                     LPROF(k, 3);
                     if (tr0) STAMP(k, 11);
