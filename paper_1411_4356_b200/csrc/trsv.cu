@@ -114,18 +114,15 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {   //
         : "memory");
     return ok != 0;
 }
-// try_wait's suspend-time hint: a waiting thread may be parked (no issue slots) until the
-// phase completes or this many ns pass
-constexpr uint32_t kSuspendNs = 20000;
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
         "@!p bra WAIT_%=;\n"
         "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity), "r"(kSuspendNs)
+        "r"(parity)
         : "memory");
 }
 
@@ -617,16 +614,19 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     mbar_arrive(xfull + k % C::kRing);   // every lane releases its own x_k[lane]
                     TPROF(k, 6);
                     if (trace && lane == 0) STAMP(k, 3);
-                } else if (tw == 1) {
-                    // x_k to every lieutenant's ring (st.async completes 16 bytes of its xbar)
+                } else {
+                    // x_k to the lieutenants' rings (st.async completes 16 bytes of its xbar):
+                    // team warp tw serves lieutenants tw-1, tw-1 + (kTeam-1), ...
                     const uint32_t off = (uint32_t)((((int64_t)k * B + lane) & (C::kRingLt * B - 1)) * 16);
                     const uint32_t bar = (uint32_t)((k % C::kRingLt) * 8);
 #pragma unroll
-                    for (int l = 0; l < C::kLt; l++) st_async2(peer_ring[l] + off, xk, peer_xbar[l] + bar);
-                    if (lane == 0)   // the single arrival of the phase, expecting the block's bytes
-#pragma unroll
-                        for (int l = 0; l < C::kLt; l++) mbar_arrive_expect_tx_remote(peer_xbar[l] + bar, B * 16);
-                    if (trace && lane == 0) STAMP(k, 8);
+                    for (int l = 0; l < C::kLt; l++)
+                        if (l % (C::kTeam - 1) == tw - 1) {
+                            if (lane == 0)   // the single arrival of the phase, expecting the block's bytes
+                                mbar_arrive_expect_tx_remote(peer_xbar[l] + bar, B * 16);
+                            st_async2(peer_ring[l] + off, xk, peer_xbar[l] + bar);
+                        }
+                    if (trace && tw == 1 && lane == 0) STAMP(k, 8);
                 }
                 xw[lane] = xk;   // my x_k: the carry of block k+3
                 __syncwarp();

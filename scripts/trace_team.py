@@ -34,8 +34,8 @@ def main():
         d = {f"{NAMES[i - 1]}->{NAMES[i]}": float(np.median(tr[:, i] - tr[:, i - 1])) for i in range(1, 8)}
         for a_, b_, nm_ in SLACK:
             d[nm_] = float(np.median(tr[:, b_] - tr[:, a_]))
-        d["end->next start (same team)"] = float(np.median(tr[2:, 0] - tr[:-2, 7]))
-        d["two steps (same team)"] = float(np.median(tr[2:, 0] - tr[:-2, 0]))
+        d["end->next start (same team)"] = float(np.median(tr[3:, 0] - tr[:-3, 7]))
+        d["three steps (same team)"] = float(np.median(tr[3:, 0] - tr[:-3, 0]))
         out[nm] = d
     print(json.dumps(out, indent=1))
     s.close()

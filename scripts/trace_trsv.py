@@ -60,7 +60,8 @@ def main():
             "lt_stage_ready_ns": med(rel[:, 12] - done_prev),
             "lt_late_landed_ns": med(rel[:, 7] - done_prev),
             "producer_static_issued_ns": med(rel[:, 9] - done_prev),
-            "lt_late_landed_minus_push_km4_ns": med(tr[4:, 7] - tr[:-4, 8]),
+            "lt_late_landed_minus_push_km3_ns": med(tr[3:, 7] - tr[:-3, 8]),
+            "lt_early_done_minus_push_km4_ns": med(tr[4:, 11] - tr[:-4, 8]),
             "lt6_q_sent_ns": med(rel[:, 2] - done_prev),
             "lt_q_sent_ns": med(rel[:, 9] - done_prev),
             "team_q_landed_ns": med(rel[:, 6] - done_prev),
