@@ -595,6 +595,9 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                 tpart[(pq * C::kTeam + tw) * B + lane] = cadd(cadd(p0, p1), cadd(p2, p3));
                 mbar_arrive(pready + pq);   // every lane, after its own partial
                 TPROF(k, 3);
+                // only warps 0 (ring) and 1 (lieutenants) need x_k (and, with kDense >= 3, every
+                // warp for its x_{k-3} carry): the others go on to their next block
+                if (kDense < 3 && tw >= 2) continue;
                 // y_k - sum_l q_l (the lieutenants' D_k^{-1}-multiplied partials), overlapping the
                 // other warps' partials
                 mbar_wait(pbar + k % C::kPbuf, (uint32_t)((k / C::kPbuf) & 1));
@@ -614,22 +617,22 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     mbar_arrive(xfull + k % C::kRing);   // every lane releases its own x_k[lane]
                     TPROF(k, 6);
                     if (trace && lane == 0) STAMP(k, 3);
-                } else {
-                    // x_k to the lieutenants' rings (st.async completes 16 bytes of its xbar):
-                    // team warp tw serves lieutenants tw-1, tw-1 + (kTeam-1), ...
+                } else if (tw == 1) {
+                    // x_k to every lieutenant's ring (st.async completes 16 bytes of its xbar)
                     const uint32_t off = (uint32_t)((((int64_t)k * B + lane) & (C::kRingLt * B - 1)) * 16);
                     const uint32_t bar = (uint32_t)((k % C::kRingLt) * 8);
 #pragma unroll
-                    for (int l = 0; l < C::kLt; l++)
-                        if (l % (C::kTeam - 1) == tw - 1) {
-                            if (lane == 0)   // the single arrival of the phase, expecting the block's bytes
-                                mbar_arrive_expect_tx_remote(peer_xbar[l] + bar, B * 16);
-                            st_async2(peer_ring[l] + off, xk, peer_xbar[l] + bar);
-                        }
-                    if (trace && tw == 1 && lane == 0) STAMP(k, 8);
+                    for (int l = 0; l < C::kLt; l++) {
+                        if (lane == 0)   // the single arrival of the phase, expecting the block's bytes
+                            mbar_arrive_expect_tx_remote(peer_xbar[l] + bar, B * 16);
+                        st_async2(peer_ring[l] + off, xk, peer_xbar[l] + bar);
+                    }
+                    if (trace && lane == 0) STAMP(k, 8);
                 }
-                xw[lane] = xk;   // my x_k: the carry of block k+3
-                __syncwarp();
+                if constexpr (kDense >= 3) {
+                    xw[lane] = xk;   // my x_k: the carry of block k+3
+                    __syncwarp();
+                }
                 TPROF(k, 7);
             }
         } else if (!chain) {
