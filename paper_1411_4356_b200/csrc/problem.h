@@ -83,7 +83,6 @@ struct TriArgs {
     const double2* nvalB;
     const int32_t* nlocB;
     const double2* dinv;      // [nblk][B(B+1)/2] inverse diagonal blocks, packed lower, column-major
-    const double2* dinvl;     // [nblk][kLt][lt_rows][B] D_k^{-1}[i, l + kLt m] (0 above the diagonal)
     const double2* G;         // [nblk][kDense][B*B] D_k^{-1} T_{k,k-d}, d = 1 .. kDense, column-major
     double2* yfar;            // [nblk*B] y_k = D_k^{-1} (b_k - far part), written by the helper CTAs
     const int64_t* operm;     // [n] output permutation out[operm[i]] = x[i] (ILUTP columns), or null
@@ -99,7 +98,6 @@ struct DevBlockTri {
     double2* fval = nullptr;
     NearDev nearB;
     double2* dinv = nullptr;
-    double2* dinvl = nullptr;
     double2* G = nullptr;
     double2* yfar = nullptr;
     uint32_t* fflag = nullptr;
@@ -111,7 +109,7 @@ struct DevBlockTri {
     int64_t nlev = 0;   // row-level dependency levels (diagnostic)
     TriArgs args() const {
         return TriArgs{n,         nblk,      rev,  B, farptr, fcol,  fval,  nearB.bp, nearB.col, nearB.val,
-                       nearB.loc, dinv,      dinvl, G,    yfar,  operm,  fflag, xfront};
+                       nearB.loc, dinv,      G,    yfar,  operm,  fflag, xfront};
     }
     void release() {
         cudaFree(farptr);
@@ -119,7 +117,6 @@ struct DevBlockTri {
         cudaFree(fval);
         nearB.release();
         cudaFree(dinv);
-        cudaFree(dinvl);
         cudaFree(G);
         cudaFree(yfar);
         cudaFree(fflag);

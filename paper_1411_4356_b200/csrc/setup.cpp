@@ -263,9 +263,7 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
     SSB_CUDA(cudaMalloc(&T.fval, std::max<int64_t>(1, nf) * sizeof(double2)));
     upload_near(HB, nB, T.nearB);
     SSB_CUDA(cudaMalloc(&T.dinv, std::max<int64_t>(1, nblk * PK) * sizeof(double2)));
-    const int LR = lt_rows(B);
-    const int64_t PL = (int64_t)kLieutenants * LR * B;   // per block: each lieutenant's columns of D^{-1}
-    SSB_CUDA(cudaMalloc(&T.dinvl, std::max<int64_t>(1, nblk * PL) * sizeof(double2)));
+
     SSB_CUDA(cudaMalloc(&T.G, std::max<int64_t>(1, nblk * kDense * B * B) * sizeof(double2)));
     SSB_CUDA(cudaMalloc(&T.yfar, std::max<int64_t>(1, nblk * B) * sizeof(double2)));
     SSB_CUDA(cudaMalloc(&T.fflag, std::max<int64_t>(1, nblk) * sizeof(uint32_t)));
@@ -324,11 +322,10 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
     // dense diagonal blocks -> explicit inverses D_k^{-1}, and Gd_k = D_k^{-1} T_{k,k-d} for
     // d = 1 .. kDense (column-major, G1 first per block), in block chunks
     const int64_t kBlkChunk = std::max<int64_t>(1, ((int64_t)1 << 27) / ((PK + kDense * (int64_t)B * B) * 16));
-    std::vector<double2> ibuf, gbuf, lbuf;
+    std::vector<double2> ibuf, gbuf;
     for (int64_t k0 = 0; k0 < nblk; k0 += kBlkChunk) {
         const int64_t k1 = std::min(nblk, k0 + kBlkChunk);
         ibuf.assign((k1 - k0) * PK, make_double2(0.0, 0.0));
-        lbuf.assign((k1 - k0) * PL, make_double2(0.0, 0.0));
         gbuf.assign((k1 - k0) * kDense * B * B, make_double2(0.0, 0.0));
         parallel_for(k1 - k0, threads, [&](int64_t lo, int64_t hi) {
             std::vector<double2> D((size_t)B * B), X((size_t)B * B), inv(B), N1((size_t)B * B);
@@ -369,13 +366,6 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
                     const int64_t cs = (int64_t)j * B - ((int64_t)j * (j - 1)) / 2;
                     for (int i = j; i < B; i++) out[cs + (i - j)] = X[(size_t)i * B + j];
                 }
-                double2* lout = &lbuf[(size_t)(k - k0) * PL];   // [l][m][i] = D^{-1}[i, l + kLt m]
-                for (int l = 0; l < kLieutenants; l++)
-                    for (int m = 0; m < LR; m++) {
-                        const int j = l + kLieutenants * m;
-                        if (j >= B) continue;
-                        for (int i = j; i < B; i++) lout[((size_t)l * LR + m) * B + i] = X[(size_t)i * B + j];
-                    }
                 // Nd = T_{k,k-d}: the distance-d entries of the block's rows; Gd = X Nd.  Row
                 // layout (ascending column): far | list B | d = kDense | .. | d = 1 | in-block
                 for (int d = 1; d <= kDense; d++) {
@@ -411,7 +401,6 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
             }
         }, 4);
         SSB_CUDA(cudaMemcpy(T.dinv + k0 * PK, ibuf.data(), (k1 - k0) * PK * sizeof(double2), cudaMemcpyHostToDevice));
-        SSB_CUDA(cudaMemcpy(T.dinvl + k0 * PL, lbuf.data(), (k1 - k0) * PL * sizeof(double2), cudaMemcpyHostToDevice));
         SSB_CUDA(cudaMemcpy(T.G + k0 * kDense * B * B, gbuf.data(), (k1 - k0) * kDense * B * B * sizeof(double2),
                             cudaMemcpyHostToDevice));
     }

@@ -64,6 +64,7 @@ __device__ __forceinline__ void st_release64(unsigned long long* p, unsigned lon
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ int ld_acq_cta(const int* p) {
     int v;
@@ -209,9 +210,9 @@ struct Cfg {
     static constexpr size_t kOffBval = kOffBcol + (size_t)kCapB * 4;
     static constexpr size_t kOffBloc = kOffBval + (size_t)kCapB * 16;
     static constexpr int kRowsL = lt_rows(B);         // rows of a block per lieutenant
-    static constexpr size_t kOffBinv = kOffBloc + (size_t)kNloc * 4;   // this lieutenant's columns of D_k^{-1}
-    static constexpr size_t kLtStage = kOffBinv + (size_t)kRowsL * B * 16;
-    static constexpr int kLtStages = 7;
+    static constexpr size_t kOffBinv = kOffBloc + (size_t)kNloc * 4;   // D_k^{-1} (packed; shared in L2 by all)
+    static constexpr size_t kLtStage = kOffBinv + (size_t)kPK * 16;
+    static constexpr int kLtStages = 6;
     static constexpr size_t kOffLtRing = kLtStage * kLtStages;   // lieutenants' x ring
     static constexpr size_t kOffLtP = kOffLtRing + (size_t)kRingLt * B * 16;   // [kLtTeams][B] row partials
     static constexpr size_t kLtRegion = kOffLtP + (size_t)kLtTeams * B * 16;
@@ -450,8 +451,10 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     unsigned char* st = sbase + stsz * s;
                     const int g = k * C::kLt + (role - 1);   // this lieutenant's rows of block k
                     stage_near(st + C::kOffBcol, st + C::kOffBval, st + C::kOffBloc, b0, b1, a.ncolB, a.nvalB,
-                               a.nlocB, g, C::kNloc, full + s, (uint32_t)(C::kRowsL * B * 16));
-                    bulk_g2s(st + C::kOffBinv, a.dinvl + (int64_t)g * C::kRowsL * B, C::kRowsL * B * 16, full + s);
+                               a.nlocB, g, C::kNloc, full + s, (uint32_t)(C::kPK * 16));
+                    // the whole packed D_k^{-1}: the helper and all seven lieutenants read the same
+                    // 8.4 KB, so DRAM sees it once (L2)
+                    bulk_g2s(st + C::kOffBinv, a.dinv + (int64_t)k * C::kPK, C::kPK * 16, full + s);
                 }
             }
         } else if (chain && warp == C::kWGProducer) {
@@ -700,11 +703,17 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     if (rowok && q < C::kTPRlate) pre(lt0, lt1, lc0, lc1, lv0, lv1);
                     // and this thread's entries of D_k^{-1} for the q product below
                     constexpr int kRows = C::kRowsL;
-                    double2 dq[kRows];   // D_k^{-1}[tt, l + kLt m] (staged zero above the diagonal)
+                    double2 dq[kRows];   // D_k^{-1}[tt, l + kLt m] (predicated: 0 above the diagonal)
                     if (tt < B) {
                         const double2* sInv = reinterpret_cast<const double2*>(st + C::kOffBinv);
 #pragma unroll
-                        for (int m = 0; m < kRows; m++) dq[m] = sInv[m * B + tt];
+                        for (int m = 0; m < kRows; m++) {
+                            const int rr = m * C::kLt + l;
+                            const bool ok = rr <= tt;
+                            dq[m] = sInv[ok ? rr * B - (rr * (rr - 1)) / 2 + (tt - rr) : 0];
+                            dq[m].x = ok ? dq[m].x : 0.0;
+                            dq[m].y = ok ? dq[m].y : 0.0;
+                        }
                     }
                     LPROF(k, 3);
                     if (tr0) STAMP(k, 11);
