@@ -159,6 +159,11 @@ def cpu_baseline(name: str, budget_s: float = 20.0):
                       f"(n={p.liouvillian_dim}) after an untimed oracle setup; {dt:.1f} s, 1 thread"}
 
 
+# oracle GMRES iterations to tol from x0 = 0 (tests/test_oracle_gmres.py, oracle.steadystate);
+# the reference arm's ms_per_step is that many steps at its sampled rate
+ORACLE_ITERATIONS = {"tiny": 11, "small": 26}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -171,8 +176,13 @@ def run_reference(args):
         if step >= args.warmup:
             vals.append(cb["value"])
     v = statistics.mean(vals)
+    # a step of the b200 arm is one solve of the workload from x0 = 0; the oracle's time for
+    # it at the sampled rate (iterations per solve from the oracle's own full solve count,
+    # one restart cycle: configs[1] converges in 26)
+    its = ORACLE_ITERATIONS.get(args.workload)
+    ms_step = 1e3 * its / v if its else None
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "iterations/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
             "config": workload_config(args.workload, base, world),
             "cpu_baseline": {**cb, "value": v},
