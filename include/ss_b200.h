@@ -172,13 +172,14 @@ int ss_precond(ss_problem* h, int32_t which, const void* x_dev, void* y_dev);
 
 /* Diagnostic: run the block substitution of factor `which` (0 = L, 1 = U) on x_dev -> y_dev
  * (device pointers, length n) with per-block %globaltimer stamps (ns) copied to host_trace
- * [SS_TRACE_STAMPS * nblk], row k (block k): 0 chain team: partials and y_k ready, 1 y_k
- * stored, 2 y warps start block k, 3 x_k stored, 4 helper: far part r_k published,
- * 5 producer saw the r_k flag, 6 y warps: lieutenant partials landed, 7 lieutenant 0:
- * x_{k-4} landed, 8 publisher: x_k pushed to the lieutenants, 9 lieutenant 0: partial sent,
- * 10 chain team: tail of step k done, 11 y warps: distance-3 product done, 12 lieutenant 0:
- * stage of block k ready, 13-15 zero.  *nblk_out receives the number of blocks
- * (host_trace may be NULL to query it). */
+ * [SS_TRACE_STAMPS * nblk], row k (block k): 0 chain team: partials of block k reduced,
+ * 2 lieutenant 6: its q_k sent, 3 x_k stored in the chain ring, 4 helper: y_k published,
+ * 5 producer: y_k staged (flag seen), 6 chain team: the lieutenants' q_k landed,
+ * 7 lieutenant 0: x_{k-3} landed, 8 chain team: x_k pushed to the lieutenants,
+ * 9 lieutenant 0: q_k sent, 10 chain team: off-chain work of block k done, 11 lieutenant
+ * 0: early part done, 12 lieutenant 0: stage of block k ready, 13 chain team: x_{k-1}
+ * read; 1, 14, 15 zero.  *nblk_out receives the number of blocks (host_trace may be NULL
+ * to query it). */
 #define SS_TRACE_STAMPS 16
 int ss_debug_trace_trsv(ss_problem* h, int32_t which, const void* x_dev, void* y_dev, uint64_t* host_trace,
                         int64_t* nblk_out);

@@ -203,8 +203,8 @@ void ilut_factor(const HostCSR& A, double drop_tol, double fill_factor, double p
 // spmv.cu
 void spmv(const DevCSR& A, const double2* x, double2* y, cudaStream_t s);
 // trsv.cu: x = T^{-1} b for one factor (b, x in natural index order; x must not alias b)
-// trace (optional, device, 8 x nblk globaltimer stamps per block): start, warp-0 far
-// done, all far done, near done, x stored, flag released, inverse staged, mat-vec done.
+// trace (optional, device, SS_TRACE_STAMPS x nblk %globaltimer stamps per block; the
+// meaning of each stamp is listed at ss_debug_trace_trsv in include/ss_b200.h).
 void block_trsv(DevBlockTri& T, const double2* b, double2* x, cudaStream_t s,
                 unsigned long long* trace = nullptr);
 size_t block_trsv_packed(int B);

@@ -178,6 +178,9 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
     // A row's entries in ascending column: far | list B (late part last) | G_kDense .. G_1 | block.
     constexpr int kD1 = kDense + 1;
     const int qmax = std::max(kD1, std::min(kMaxQ, q_max));
+    // per-lieutenant entry budget of a block: the stage capacity, or less (SSB_TRSV_LTCAP) to
+    // keep heavy blocks from making their lieutenants late (the rest goes to the helpers)
+    const int ltcap = std::min(near_cap_b(B), env_int("SSB_TRSV_LTCAP", near_cap_b(B)));
     std::vector<int> qk(nblk, qmax);
     parallel_for(nblk, threads, [&](int64_t lo, int64_t hi) {
         for (int64_t k = lo; k < hi; k++) {
@@ -187,7 +190,7 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
                 for (int64_t ip = k * B; ip < std::min(n, (k + 1) * B); ip++)
                     for (int d = kD1; d < q; d++) cb[(ip - k * B) % kLieutenants] += dcnt[(size_t)ip * kMaxQ + d];
                 bool fit = true;
-                for (int l = 0; l < kLieutenants; l++) fit = fit && cb[l] + 3 <= near_cap_b(B);
+                for (int l = 0; l < kLieutenants; l++) fit = fit && cb[l] + 3 <= ltcap;
                 if (fit) break;
             }
             qk[k] = q;

@@ -361,10 +361,9 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
     uint64_t* rfull = reinterpret_cast<uint64_t*>(smem + C::kOffRfull);   // chain: r_k staged
     double2* tpart = reinterpret_cast<double2*>(smem + C::kOffTpart);
     uint64_t* pready = reinterpret_cast<uint64_t*>(smem + C::kOffPready);
-    int* sDone = reinterpret_cast<int*>(smem + C::kOffInts);   // chain: blocks of x done
-    int* sF = sDone + 1;                                          // helpers: frontier view
-    int* sLock = sDone + 2;
-    int* sPub = sDone + 3;                                        // chain: blocks published
+    int* sF = reinterpret_cast<int*>(smem + C::kOffInts);      // helpers: frontier view
+    int* sLock = sF + 1;
+    int* sPub = sF + 2;                                           // chain: blocks published
     double2* ring = reinterpret_cast<double2*>(smem + C::kOffRing);
     double2* pbuf = reinterpret_cast<double2*>(smem + C::kOffPbuf);
     constexpr int kRingMask = C::kRing * B - 1;
@@ -391,7 +390,6 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
         for (int j = 0; j < C::kPbuf; j++) mbar_init(pbar + j, 1);
         for (int j = 0; j < C::kRing; j++) mbar_init(xfull + j, 32);   // the 32 lanes of the storing warp
         for (int j = 0; j < 4; j++) mbar_init(pready + j, C::kTeam * 32);   // every lane of a team
-        *sDone = 0;
         *sF = 0;
         *sLock = 0;
         *sPub = 0;

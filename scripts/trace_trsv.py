@@ -1,6 +1,6 @@
-"""Critical-path breakdown of the block substitution (trsv.cu) from %globaltimer stamps
-(per block: chain data ready, near done, mat-vec done, x stored; helper far published;
-producer saw the flag; frontier published; helper start).
+"""Critical-path breakdown of the block substitution (trsv.cu) from the %globaltimer
+stamps of ss_debug_trace_trsv (include/ss_b200.h lists them): chain team, lieutenants,
+helpers and producer per block, relative to the previous block's x being stored.
 
 usage: python scripts/trace_trsv.py NAME [field=value ...]
 For each factor prints medians (ns) of the chain step and its parts, and how far the
@@ -45,26 +45,21 @@ def main():
             "step_pct_ns": [float(v) for v in np.percentile(step, [10, 50, 90, 99])],
             "excess_us": float(ex.sum() / 1e3),
             "excess_helper_late_us": float(np.sum(np.where(rel[:, 5] > done_prev - 2000, ex, 0)) / 1e3),
-            # chain team (relative to x_{k-1} stored)
-            "team_tail_done_ns": med(rel[:, 10] - done_prev),
-            "team_ready_ns": med(rel[:, 0] - done_prev),
+            # chain team of block k (relative to x_{k-1} stored)
+            "team_offchain_done_ns": med(rel[:, 10] - done_prev),
+            "team_read_xprev_ns": med(rel[:, 13] - done_prev),
+            "team_q_landed_ns": med(rel[:, 6] - done_prev),
+            "team_reduced_ns": med(rel[:, 0] - done_prev),
             "team_reduce_store_ns": med(tr[:, 3] - tr[:, 0]),
             "team_push_minus_store_ns": med(tr[:, 8] - tr[:, 3]),
-            # y warps
-            "y_stage_ready_ns": med(rel[:, 2] - done_prev),
-            "y_pbar_ns": med(rel[:, 6] - done_prev),
-            "team_g1_loaded_ns": med(rel[:, 13] - done_prev),
-            "lt_early_done_ns": med(rel[:, 11] - done_prev),
-            "y_done_ns": med(rel[:, 1] - done_prev),
-            # lieutenant 0 (relative to x_{k-1} stored)
+            # lieutenants (relative to x_{k-1} stored)
             "lt_stage_ready_ns": med(rel[:, 12] - done_prev),
+            "lt_early_done_ns": med(rel[:, 11] - done_prev),
             "lt_late_landed_ns": med(rel[:, 7] - done_prev),
-            "producer_static_issued_ns": med(rel[:, 9] - done_prev),
+            "lt_q_sent_ns": med(rel[:, 9] - done_prev),
+            "lt6_q_sent_ns": med(rel[:, 2] - done_prev),
             "lt_late_landed_minus_push_km3_ns": med(tr[3:, 7] - tr[:-3, 8]),
             "lt_early_done_minus_push_km4_ns": med(tr[4:, 11] - tr[:-4, 8]),
-            "lt6_q_sent_ns": med(rel[:, 2] - done_prev),
-            "lt_q_sent_ns": med(rel[:, 9] - done_prev),
-            "team_q_landed_ns": med(rel[:, 6] - done_prev),
             # helpers / producer
             "helper_publish_ns": med(rel[:, 4] - done_prev),
             "producer_flag_pct_ns": [float(v) for v in np.percentile(rel[:, 5] - done_prev, [10, 50, 90, 99])],
@@ -74,8 +69,8 @@ def main():
         if slow.any():
             d["slow_steps"] = int(slow.sum())
             d["slow_team_offchain_done_ns"] = med((rel[:, 10] - done_prev)[slow])
-            d["slow_team_saw_prev_ns"] = med((rel[:, 13] - done_prev)[slow])
-            d["slow_team_ready_ns"] = med((rel[:, 0] - done_prev)[slow])
+            d["slow_team_read_xprev_ns"] = med((rel[:, 13] - done_prev)[slow])
+            d["slow_team_reduced_ns"] = med((rel[:, 0] - done_prev)[slow])
             d["slow_lt_late_landed_ns"] = med((rel[:, 7] - done_prev)[slow])
             d["slow_producer_flag_ns"] = med((rel[:, 5] - done_prev)[slow])
         out[nm] = d

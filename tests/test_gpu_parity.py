@@ -228,7 +228,7 @@ def test_trace_abi(cuda):
     y = torch.empty_like(x)
     tr = pb().ss_debug_trace_trsv(s.handle, 0, x.data_ptr(), y.data_ptr())
     assert tr.shape == ((s.n + 31) // 32, 16)
-    assert np.all(tr[:, 3] > 0)
+    assert np.all(tr[:, 3] > 0) and np.all(tr[:, 14:] == 0)
     ref = s.precond(x, 0)
     assert torch.equal(y, ref)      # tracing does not change the result
     s.close()
