@@ -436,6 +436,7 @@ void setup_problem(Problem& P, double drop_tol, double fill_factor, double permt
     if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
     const int B = env_int("SSB_TRSV_B", 32);
     const int QMAX = env_int("SSB_TRSV_Q", 32);
+    const int QMAX_U = env_int("SSB_TRSV_QU", QMAX);   // (the upper factor's window, if different)
     int64_t levL = 0, levU = 0;
     std::thread lev([&] {
         levL = count_levels(P.hL, false);
@@ -443,7 +444,7 @@ void setup_problem(Problem& P, double drop_tol, double fill_factor, double permt
     });
     try {
         build_block_tri(P.hL, false, B, QMAX, threads, P.L, s);
-        build_block_tri(P.hU, true, B, QMAX, threads, P.U, s);
+        build_block_tri(P.hU, true, B, QMAX_U, threads, P.U, s);
         bool identity = true;
         for (int64_t q = 0; q < P.n && identity; q++) identity = P.colperm[q] == q;
         if (!identity) {   // ILUTP exchanged columns: the U substitution scatters x = Pi y
