@@ -232,3 +232,58 @@ def test_trace_abi(cuda):
     ref = s.precond(x, 0)
     assert torch.equal(y, ref)      # tracing does not change the result
     s.close()
+
+
+def test_full_size_medium(cuda):
+    """BASELINE configs[2] (n = 360,000) at full size through the C ABI, in the launch
+    configuration bench.py times: properties that hold at any size (the oracle's direct
+    solve does not fit here) -- the north-star residual of the GPU steady state computed
+    with the oracle's own Liouvillian, Tr rho = 1, rho = rho^H, a real non-negative
+    diagonal -- and the forward substitution checked row by row on sampled rows against
+    its plain definition (y_i + sum_{j<i} l_ij y_j = x_i) with the exported factor."""
+    torch = cuda
+    p = CONFIGS["medium"]
+    s = pb().SteadyState(p).setup().solve()
+    info = s.solve_info
+    assert info["converged"] == 1 and info["rel_residual"] <= p.tol
+    rho = s.rho().cpu().numpy()
+    assert ss.liouvillian_residual(rho, p) <= 1e-9
+    assert abs(np.trace(rho) - 1) <= 1e-12
+    # the exact steady state is Hermitian with a real non-negative diagonal, so these
+    # deviations are bounded by 2 ||rho - rho_exact||_1, which the north star bounds by
+    # 2e-6 (measured: 7e-10)
+    assert np.abs(rho - rho.conj().T).sum() <= 2e-6
+    d = np.diag(rho)
+    assert np.abs(d.imag).sum() <= 2e-6 and d.real.min() >= -2e-6
+    # forward substitution, sampled rows (position space of the RCM-permuted system)
+    n = s.n
+    x = rand_cvec(n, 21)
+    y = s.precond(torch.from_numpy(x).cuda(), 0).cpu().numpy()
+    rp, ci, va = pb().ss_export_factors(s.handle, 0)
+    rng = np.random.default_rng(5)
+    rows = np.unique(np.concatenate([rng.integers(0, n, 400), [0, 1, 31, 32, n - 33, n - 1]]))
+    for i in rows:
+        lhs = y[i] + np.dot(va[rp[i]:rp[i + 1]], y[ci[rp[i]:rp[i + 1]]])
+        assert abs(lhs - x[i]) <= 1e-10 * (np.abs(x).max() + np.abs(y).max())
+    s.close()
+
+
+def test_full_size_sweep_points(cuda):
+    """BASELINE configs[4] (n = 230,400 per point) at full size through the sweep driver
+    (sweep.py, world size 1) on the two end points of the detuning range.  Delta = -2
+    converges to the BASELINE tolerance (north-star residual recomputed by the oracle's
+    Liouvillian, Tr rho = 1; the oracle's direct solve does not fit at this size).  At
+    Delta = +2 the iLUTP factors with the sweep's d, p are unstable (reading R15): the
+    driver must report the breakdown (converged = 0) for that point and carry on."""
+    from paper_1411_4356_b200.sweep import run_sweep
+    from workloads import sweep_params
+    pts = [sweep_params()[0], sweep_params()[-1]]
+    table = run_sweep(pts)
+    assert table[0][0] == pts[0].Delta and table[0][5] == 1.0 and table[0][4] <= pts[0].tol
+    assert table[1][0] == pts[1].Delta and table[1][5] == 0.0
+    s = pb().SteadyState(pts[0]).setup().solve()
+    rho = s.rho().cpu().numpy()
+    assert ss.liouvillian_residual(rho, pts[0]) <= 1e-9 and abs(np.trace(rho) - 1) <= 1e-12
+    na, nb = s.expect()
+    assert abs(na - table[0][1]) <= 1e-12 and abs(nb - table[0][2]) <= 1e-12   # the driver's numbers
+    s.close()
