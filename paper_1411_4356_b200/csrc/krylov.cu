@@ -14,8 +14,11 @@
 // is staged in shared memory, the update uses it, the dot products re-use it, so V
 // is read from HBM once per pass.  Reductions are two-stage with a fixed order
 // (block partials, then one block per output) -- deterministic, no atomics.
-// The 1-thread Hessenberg/Givens step runs on the device; the host only reads one
-// status word per Arnoldi step to decide whether to stop.
+// The 1-thread Hessenberg/Givens step runs on the device; the host reads one status word
+// per Arnoldi step to decide whether to stop.  While it waits for step j's status, step
+// j+1 is already enqueued (speculatively, unless step j's predecessor was within a factor
+// kSpecMargin of the stopping target): the device never idles on the host round trip, and
+// a speculative step behind the last one is simply not used (same steps, same result).
 #include <cstdio>
 
 #include "problem.h"
@@ -292,6 +295,7 @@ void ensure_krylov(Problem& P, int m) {
     SSB_CUDA(cudaMalloc(&K.hcol, words * sizeof(double2)));
     SSB_CUDA(cudaMalloc(&K.scal, 8 * sizeof(double)));
     SSB_CUDA(cudaHostAlloc(&K.h_stat, 8 * sizeof(double), cudaHostAllocDefault));
+    for (auto& e : K.st_ev) SSB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     static bool attr_set = false;
     if (!attr_set) {
         SSB_CUDA(cudaFuncSetAttribute(k_cgs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cgs_smem(kMaxVec)));
@@ -375,7 +379,8 @@ void gmres_solve(Problem& P, const double2* b_dev, int m, double tol, int max_it
         if (!(beta > 0.0) || !std::isfinite(beta)) break;
         const double target = beta * tol * bnorm / rn;
         int k = 0;
-        for (int j = 0; j < m; j++) {
+        // enqueue Arnoldi step j (+ its status copy into slot j & 1); V_j must be in place
+        auto enqueue_step = [&](int j) {
             double2* vj = K.V + (int64_t)j * n;
             spmv(P.A, vj, K.t, s);
             apply_precond(P, K.t, K.w, K.r, s);
@@ -391,15 +396,34 @@ void gmres_solve(Problem& P, const double2* b_dev, int m, double tol, int max_it
             launch_reduce(c, nv + 1, nv, 1, c.st.nrm);
             k_arnoldi_step<<<1, 1, 0, s>>>(c.st, m, j);
             SSB_LAUNCHED();
-            SSB_CUDA(cudaMemcpyAsync(K.h_stat, K.scal, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
-            SSB_CUDA(cudaStreamSynchronize(s));
-            total++;
-            k = j + 1;
-            const double est = K.h_stat[0], hn = K.h_stat[1];
-            const bool breakdown = K.h_stat[3] != 0.0 || !(hn > 0.0) || !std::isfinite(est);
-            if (est <= target || total >= max_iter || breakdown || j == m - 1) break;
+            SSB_CUDA(cudaMemcpyAsync(K.h_stat + 4 * (j & 1), K.scal, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+            SSB_CUDA(cudaEventRecord(K.st_ev[j & 1], s));
+        };
+        auto enqueue_next_vector = [&](int j) {   // V_{j+1} = w / h_{j+1,j}
             k_scale<<<grid1(n), 256, 0, s>>>(K.w, K.V + (int64_t)(j + 1) * n, n, K.scal + 2, nullptr);
             SSB_LAUNCHED();
+        };
+        constexpr double kSpecMargin = 8.0;   // (the estimate falls ~2.4x per step on configs[1])
+        double prev_est = INFINITY;   // Givens estimate of the step before
+        bool queued = false;          // step j is already enqueued
+        for (int j = 0; j < m; j++) {
+            if (!queued) enqueue_step(j);
+            // speculate step j+1 while step j's status travels to the host
+            const bool spec = j + 1 < m && total + 1 < max_iter && prev_est > kSpecMargin * target;
+            if (spec) {
+                enqueue_next_vector(j);
+                enqueue_step(j + 1);
+            }
+            SSB_CUDA(cudaEventSynchronize(K.st_ev[j & 1]));
+            const double* st = K.h_stat + 4 * (j & 1);
+            total++;
+            k = j + 1;
+            const double est = st[0], hn = st[1];
+            const bool breakdown = st[3] != 0.0 || !(hn > 0.0) || !std::isfinite(est);
+            if (est <= target || total >= max_iter || breakdown || j == m - 1) break;   // a speculative step j+1 is unused
+            if (!spec) enqueue_next_vector(j);
+            queued = spec;
+            prev_est = est;
         }
         k_backsolve<<<1, 1, 0, s>>>(c.st, m, k);
         SSB_LAUNCHED();

@@ -141,7 +141,8 @@ struct Krylov {
     int part_cap = 0;
     double2* hcol = nullptr;   // device Hessenberg column accumulators (2 x (m+2))
     double* scal = nullptr;    // device scalars
-    double* h_stat = nullptr;  // pinned host mirror of scalars
+    double* h_stat = nullptr;  // pinned host mirror of scalars (two 4-double slots: steps j, j+1)
+    cudaEvent_t st_ev[2] = {nullptr, nullptr};   // the status copy of step j landed (slot j & 1)
     void release() {
         cudaFree(V);
         cudaFree(w);
@@ -153,6 +154,8 @@ struct Krylov {
         cudaFree(hcol);
         cudaFree(scal);
         if (h_stat) cudaFreeHost(h_stat);
+        for (auto& e : st_ev)
+            if (e) cudaEventDestroy(e);
         *this = Krylov();
     }
 };
