@@ -26,10 +26,23 @@
 // serial algorithm, so the factors are bit-identical for any thread count.  U rows are
 // kept in original columns while factoring (later exchanges move positions > i) and
 // converted to final positions at the end.
+//
+// The chain of row hand-offs (row i needs U row i-1) is the critical path, so the work
+// between "F reaches i" and "U row i published" is kept small: the row's positions live in
+// a bitmap (elimination order = ascending set bits, no heaps), the U candidates are
+// snapshotted while the last kSnapAhead rows are still being finished elsewhere and kept
+// current by the late updates, the cap is a counting selection over binary orders of
+// magnitude, the U row is published in position order as selected, and the L row, the
+// clearing of the work row and the arena page faults are done after publication.
+// SSB_ILUT_PROF=1 prints the per-row time of each phase.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <thread>
 
@@ -39,6 +52,12 @@
 #else
 #define SSB_PAUSE() std::this_thread::yield()
 #endif
+// spin, and give the core away now and then (another thread may own the next row)
+#define SSB_BACKOFF(cnt)                                 \
+    do {                                                 \
+        if (((++(cnt)) & 255) == 0) std::this_thread::yield(); \
+        else SSB_PAUSE();                                \
+    } while (0)
 
 #include "problem.h"
 
@@ -51,24 +70,36 @@ inline double mag2(double2 z) { return z.x * z.x + z.y * z.y; }
 // append-only storage whose blocks never move (other threads read published rows)
 struct Arena {
     static constexpr int64_t kBlock = 1 << 20;
-    std::vector<std::unique_ptr<int64_t[]>> cblocks;
+    std::vector<std::unique_ptr<int32_t[]>> cblocks;
     std::vector<std::unique_ptr<double2[]>> vblocks;
-    int64_t used = kBlock;
-    void reserve(int64_t len, int64_t*& c, double2*& v) {
-        if (cblocks.empty() || used + len > kBlock) {
-            int64_t sz = std::max(kBlock, len);
-            cblocks.emplace_back(new int64_t[sz]);
-            vblocks.emplace_back(new double2[sz]);
-            used = 0;
-        }
+    int64_t used = kBlock, size = 0;
+    int64_t touched = 0;   // entries of the current block whose pages were written
+    void grow(int64_t len) {
+        size = std::max(kBlock, len);
+        cblocks.emplace_back(new int32_t[size]);
+        vblocks.emplace_back(new double2[size]);
+        used = touched = 0;
+    }
+    void reserve(int64_t len, int32_t*& c, double2*& v) {
+        if (cblocks.empty() || used + len > size) grow(len);
         c = cblocks.back().get() + used;
         v = vblocks.back().get() + used;
         used += len;
     }
+    // take the page faults of the next `ahead` entries now (off the critical path)
+    void prefault(int64_t ahead) {
+        if (cblocks.empty() || used + ahead > size) grow(ahead);
+        const int64_t end = std::min(size, used + ahead);
+        int32_t* c = cblocks.back().get();
+        double2* v = vblocks.back().get();
+        for (int64_t e = std::max(touched, used); e < end; e += 256) v[e] = make_double2(0.0, 0.0);   // 4 KB
+        for (int64_t e = std::max(touched, used); e < end; e += 1024) c[e] = 0;
+        touched = std::max(touched, end);
+    }
 };
 
 struct RowRef {
-    const int64_t* c = nullptr;
+    const int32_t* c = nullptr;   // int32: n < 2^31 (checked), fewer bytes per re-read U row
     const double2* v = nullptr;
     int64_t len = 0;
 };
@@ -92,39 +123,167 @@ struct Shared {
     std::vector<RowRef> Lrow, Urow;                   // L: positions; U: original columns
     std::atomic<int> error_row{-1};
     std::atomic<int32_t> repaired{0}, swaps{0};
+    bool prof = false;                                // SSB_ILUT_PROF: per-phase times (stderr)
+    std::atomic<int64_t> t_elim{0}, t_spin{0}, t_wait{0}, t_fin{0}, n_late{0}, t_post{0}, n_cand{0}, n_lcand{0},
+        t_fcand{0}, t_fsel{0}, n_kept{0}, n_snap{0};
     explicit Shared(const HostCSR& a) : A(a) {}
 };
+
+constexpr int64_t kSnapAhead = 2;   // snapshot the U candidates once F >= i - kSnapAhead
+
+// next set bit of b in [from, lim), else lim
+inline int64_t next_bit(const uint64_t* b, int64_t from, int64_t lim) {
+    if (from >= lim) return lim;
+    int64_t wi = from >> 6;
+    uint64_t x = b[wi] & (~0ull << (from & 63));
+    for (;;) {
+        if (x) {
+            const int64_t p = (wi << 6) + __builtin_ctzll(x);
+            return p < lim ? p : lim;
+        }
+        if ((++wi << 6) >= lim) return lim;
+        x = b[wi];
+    }
+}
+
+// the k-th largest of m[0..cnt) (1 <= k < cnt; all m > 0): one counting pass over binary
+// orders of magnitude, then a selection inside the one bucket that holds it
+inline double kth_largest(const double* m, size_t cnt, int64_t k, std::vector<double>& tmp) {
+    constexpr int kBins = 128;
+    uint32_t hist[kBins] = {};
+    auto bexp = [](double x) {
+        uint64_t b;
+        std::memcpy(&b, &x, 8);
+        return (int)(b >> 52);   // x >= 0: sign bit clear
+    };
+    int emax = 0;
+    for (size_t t = 0; t < cnt; t++) emax = std::max(emax, bexp(m[t]));
+    auto bin = [&](double x) { return std::min(kBins - 1, emax - bexp(x)); };   // 0 = largest
+    for (size_t t = 0; t < cnt; t++) hist[bin(m[t])]++;
+    int b = 0;
+    int64_t above = 0;
+    while (above + hist[b] < k) above += hist[b++];
+    tmp.clear();
+    for (size_t t = 0; t < cnt; t++)
+        if (bin(m[t]) == b) tmp.push_back(m[t]);
+    const int64_t r = k - above;   // 1 <= r <= hist[b]
+    std::nth_element(tmp.begin(), tmp.begin() + (r - 1), tmp.end(), std::greater<double>());
+    return tmp[r - 1];
+}
 
 void worker(Shared& S, Arena& La, Arena& Ua) {
     const int64_t n = S.n;
     std::vector<double2> w(n, make_double2(0.0, 0.0));   // indexed by ORIGINAL column
     std::vector<uint8_t> present(n, 0);
-    std::vector<int64_t> nz, heap;
-    std::vector<std::pair<int64_t, int64_t>> pending;   // min-heap of (position when keyed, column)
+    // the row's columns by POSITION: bit p set = the column at position p is in the row.
+    // Positions are eliminated in increasing order by scanning the bits (fill from U row k
+    // lies at positions > k), the U part is the bits >= i.
+    std::vector<uint64_t> bits(((size_t)n >> 6) + 2, 0);
+    std::vector<int64_t> nz;
     std::vector<Ent> lbuf, buf;
+    std::vector<double> mk, km;
+    // U candidates of the row (positions > i): snapshot taken while the last rows before i are
+    // finished by other threads; afterwards only the entries the late U rows touch change
+    std::vector<int32_t> sidx(n, -1);   // column -> snapshot index
+    std::vector<int64_t> s_pos, s_col;
+    std::vector<double> s_m;
+    std::vector<int32_t> kidx, ties;
+    bool snapped = false;
     nz.reserve(4096);
-    pending.reserve(4096);
-    heap.reserve(4096);
     buf.reserve(4096);
     lbuf.reserve(4096);
-    auto cmp_heap = [](int64_t a, int64_t b) { return a > b; };   // min-heap of positions
-    auto cmp_pend = [](const std::pair<int64_t, int64_t>& a, const std::pair<int64_t, int64_t>& b) {
-        return a.first > b.first;
-    };
     auto by_mag = [](const Ent& a, const Ent& b) { return a.m > b.m || (a.m == b.m && a.j < b.j); };
     auto by_pos = [](const Ent& a, const Ent& b) { return a.j < b.j; };
     const double pt2 = S.permtol * S.permtol;
+    uint64_t* bt = bits.data();
+    int64_t lo = n, hi = -1;   // range of positions set in this row
+    auto setbit = [&](int64_t p) {
+        bt[p >> 6] |= 1ull << (p & 63);
+        lo = std::min(lo, p);
+        hi = std::max(hi, p);
+    };
+    auto clear_bits = [&]() {
+        if (hi >= lo) std::memset(bt + (lo >> 6), 0, (size_t)((hi >> 6) - (lo >> 6) + 1) * sizeof(uint64_t));
+        lo = n;
+        hi = -1;
+    };
 
+    auto take_snapshot = [&](int64_t i) {
+        for (int64_t pp = next_bit(bt, i + 1, hi + 1); pp <= hi; pp = next_bit(bt, pp + 1, hi + 1)) {
+            const int64_t c = S.perm[pp].load(std::memory_order_relaxed);
+            sidx[c] = (int32_t)s_col.size();
+            s_pos.push_back(pp);
+            s_col.push_back(c);
+            s_m.push_back(mag2(w[c]));
+        }
+        snapped = true;
+    };
+    auto drop_snapshot = [&]() {
+        for (int64_t c : s_col) sidx[c] = -1;
+        s_pos.clear();
+        s_col.clear();
+        s_m.clear();
+        snapped = false;
+    };
+
+    // w <- w - wk * (U row k), new fill recorded; with a snapshot (SN) also keep the
+    // magnitudes of the U candidates (positions > i) current
+    auto update_row = [&](const RowRef& U, double2 wk, int64_t i, auto sn) {
+        constexpr bool SN = decltype(sn)::value;
+        const int32_t* __restrict uc = U.c;
+        const double2* __restrict uv = U.v;
+        double2* __restrict wp = w.data();
+        uint8_t* __restrict pr = present.data();
+        const int64_t len = U.len;
+        for (int64_t q = 1; q < len; q++) {
+            const int64_t c = uc[q];
+            if (__builtin_expect(!pr[c], 0)) {   // fill: position > k (see above)
+                pr[c] = 1;
+                wp[c] = make_double2(0.0, 0.0);
+                nz.push_back(c);
+                const int64_t pc = S.iperm[c].load(std::memory_order_relaxed);
+                setbit(pc);
+                if (SN && pc > i) {
+                    sidx[c] = (int32_t)s_col.size();
+                    s_pos.push_back(pc);
+                    s_col.push_back(c);
+                    s_m.push_back(0.0);
+                }
+            }
+            const double2 u = uv[q];
+            const double px = wk.x * u.x - wk.y * u.y;
+            const double py = wk.x * u.y + wk.y * u.x;
+            double2 t = wp[c];
+            t.x = t.x - px;
+            t.y = t.y - py;
+            wp[c] = t;
+            if (SN) {
+                const int32_t si = sidx[c];
+                if (si >= 0) s_m[si] = mag2(t);
+            }
+        }
+    };
+
+    using clk = std::chrono::steady_clock;
+    auto ns = [](clk::time_point a, clk::time_point b) {
+        return (int64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(b - a).count();
+    };
+    int64_t p_elim = 0, p_spin = 0, p_wait = 0, p_fin = 0, p_late = 0, p_post = 0, p_cand = 0, p_lcand = 0;
+    int64_t p_fcand = 0, p_fsel = 0, p_kept = 0, p_snap = 0;
     for (;;) {
         const int64_t i = S.next.fetch_add(1, std::memory_order_relaxed);
         if (i >= n) break;
+        clk::time_point tp0 = S.prof ? clk::now() : clk::time_point();
         const int64_t r0 = S.A.rowptr[i], r1 = S.A.rowptr[i + 1];
         const int64_t lfil = (int64_t)(S.fill_factor * (double)(r1 - r0) / 2.0);
         double rowmax2 = 0.0;
         nz.clear();
-        pending.clear();
-        heap.clear();
         lbuf.clear();
+        // positions are read after the version: a later exchange is seen as a new version.
+        // A position read while an exchange of step s >= f0 is under way may be stale, but
+        // then both its old and new value are >= f0, hence cursor <= f0 below.
+        const int64_t f0 = S.front.load(std::memory_order_acquire);
+        int64_t my_version = S.swap_version.load(std::memory_order_acquire);
         for (int64_t q = r0; q < r1; q++) {
             const int64_t c = S.A.col[q];
             const double m = mag2(S.A.val[q]);
@@ -132,41 +291,54 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
             w[c] = S.A.val[q];
             present[c] = 1;
             nz.push_back(c);
-            pending.emplace_back(S.iperm[c].load(std::memory_order_relaxed), c);
+            setbit(S.iperm[c].load(std::memory_order_relaxed));
         }
-        std::make_heap(pending.begin(), pending.end(), cmp_pend);
-        int64_t my_version = -1;   // forces a re-key on the first pass
+        int64_t cursor = std::min(lo, f0);   // the row's positions < cursor are eliminated (or dropped)
+        uint32_t spins = 0;
         const double tau2 = S.drop_tol * S.drop_tol * rowmax2;
 
-        // eliminate final positions < min(F, i) in increasing order as F advances.  Pending
-        // columns are keyed by their position; positions only change through column
-        // exchanges, which bump swap_version before the frontier moves on, so the keys are
-        // refreshed only when that happens (rare).
+        // eliminate final positions < min(F, i) in increasing order as F advances.  Positions
+        // only change through column exchanges (step s exchanges s and t >= s >= F), which
+        // bump swap_version before the frontier moves on; the bits >= cursor are then
+        // rebuilt from the row's columns (rare).
         for (;;) {
             const int64_t f = S.front.load(std::memory_order_acquire);
             const int64_t ver = S.swap_version.load(std::memory_order_acquire);
             if (ver != my_version) {
-                for (auto& e : pending) e.first = S.iperm[e.second].load(std::memory_order_relaxed);
-                std::make_heap(pending.begin(), pending.end(), cmp_pend);
+                if (snapped) drop_snapshot();
+                const int64_t keep_lo = lo;
+                clear_bits();
+                for (int64_t c : nz) {
+                    const int64_t pc = S.iperm[c].load(std::memory_order_relaxed);
+                    if (pc >= cursor) setbit(pc);
+                }
+                lo = std::min(lo, keep_lo);   // the clearing range still covers eliminated words
+                hi = std::max(hi, cursor);
                 my_version = ver;
             }
             const int64_t lim = std::min(f, i);
-            while (!pending.empty() && pending.front().first < lim) {
-                heap.push_back(pending.front().first);
-                std::push_heap(heap.begin(), heap.end(), cmp_heap);
-                std::pop_heap(pending.begin(), pending.end(), cmp_pend);
-                pending.pop_back();
-            }
-            if (heap.empty()) {
+            int64_t k = next_bit(bt, cursor, lim);
+            if (k >= lim) {
+                cursor = std::max(cursor, lim);
                 if (f >= i) break;
                 if (S.error_row.load(std::memory_order_relaxed) >= 0) break;
-                SSB_PAUSE();
+                if (!snapped && f >= i - kSnapAhead) {
+                    take_snapshot(i);
+                    continue;
+                }
+                if (S.prof) {
+                    const auto a = clk::now();
+                    SSB_BACKOFF(spins);
+                    p_spin += ns(a, clk::now());
+                } else {
+                    SSB_BACKOFF(spins);
+                }
                 continue;
             }
-            while (!heap.empty()) {
-                std::pop_heap(heap.begin(), heap.end(), cmp_heap);
-                const int64_t k = heap.back();
-                heap.pop_back();
+            const bool late = S.prof && f >= i - 1;
+            const clk::time_point tl = late ? clk::now() : clk::time_point();
+            for (; k < lim; k = next_bit(bt, cursor, lim)) {
+                cursor = k + 1;
                 const int64_t ck = S.perm[k].load(std::memory_order_relaxed);
                 const RowRef& U = S.Urow[k];
                 const double2 ukk = U.v[0];
@@ -180,79 +352,83 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
                 }
                 w[ck] = wk;
                 lbuf.push_back(Ent{k, ck, wk, mag2(wk)});
-                for (int64_t q = 1; q < U.len; q++) {
-                    const int64_t c = U.c[q];
-                    const double2 u = U.v[q];
-                    if (!present[c]) {
-                        present[c] = 1;
-                        w[c] = make_double2(0.0, 0.0);
-                        nz.push_back(c);
-                        const int64_t p = S.iperm[c].load(std::memory_order_relaxed);
-                        if (p < lim) {
-                            heap.push_back(p);
-                            std::push_heap(heap.begin(), heap.end(), cmp_heap);
-                        } else {
-                            pending.emplace_back(p, c);
-                            std::push_heap(pending.begin(), pending.end(), cmp_pend);
-                        }
-                    }
-                    const double px = wk.x * u.x - wk.y * u.y;
-                    const double py = wk.x * u.y + wk.y * u.x;
-                    w[c].x = w[c].x - px;
-                    w[c].y = w[c].y - py;
+                if (snapped) {
+                    update_row(U, wk, i, std::true_type{});
+                } else {
+                    update_row(U, wk, i, std::false_type{});
                 }
             }
+            cursor = std::max(cursor, lim);
+            if (late) p_late += ns(tl, clk::now());
         }
         // wait until every earlier row is published (then nobody else exchanges columns)
+        clk::time_point tp1 = S.prof ? clk::now() : clk::time_point();
         while (S.front.load(std::memory_order_acquire) < i) {
             if (S.error_row.load(std::memory_order_relaxed) >= 0) break;
-            SSB_PAUSE();
+            SSB_BACKOFF(spins);
         }
+        clk::time_point tp2 = S.prof ? clk::now() : clk::time_point();
         if (S.error_row.load(std::memory_order_relaxed) >= 0) {   // drain after a breakdown
             for (int64_t c : nz) {
                 present[c] = 0;
                 w[c] = make_double2(0.0, 0.0);
             }
+            clear_bits();
+            drop_snapshot();
             S.Lrow[i] = RowRef{};
             S.Urow[i] = RowRef{};
             S.front.store(i + 1, std::memory_order_release);
             continue;
         }
 
-        // L part: multipliers kept, nonzero, above the threshold; cap; by position
-        buf.clear();
-        for (const Ent& e : lbuf) {
-            const double m = mag2(w[e.c]);
-            if (m != 0.0 && !(m < tau2)) buf.push_back(Ent{e.j, e.c, w[e.c], m});
-        }
-        if ((int64_t)buf.size() > lfil) {
-            std::nth_element(buf.begin(), buf.begin() + lfil, buf.end(), by_mag);
-            buf.resize(lfil);
-        }
-        std::sort(buf.begin(), buf.end(), by_pos);
-        {
-            int64_t* c;
-            double2* v;
-            La.reserve((int64_t)buf.size(), c, v);
-            for (size_t t = 0; t < buf.size(); t++) {
-                c[t] = buf[t].j;
-                v[t] = buf[t].v;
-            }
-            S.Lrow[i] = RowRef{c, v, (int64_t)buf.size()};
-        }
-        // U part: positions > i (pending holds exactly the columns at positions >= i)
+        // U part: the row's positions > i (current: no exchange is pending now).  With a
+        // snapshot (kept current by update_row since) nothing is re-read.
+        clk::time_point tq0 = S.prof ? clk::now() : clk::time_point();
         const int64_t cdiag = S.perm[i].load(std::memory_order_relaxed);
         double2 di = present[cdiag] ? w[cdiag] : make_double2(0.0, 0.0);
-        buf.clear();
-        for (const auto& e : pending) {
-            const int64_t c = e.second;
-            if (c == cdiag) continue;
-            const double m = mag2(w[c]);
-            if (m != 0.0 && !(m < tau2)) buf.push_back(Ent{S.iperm[c].load(std::memory_order_relaxed), c, w[c], m});
+        if (S.prof) p_snap += snapped;
+        if (!snapped) take_snapshot(i);   // else kept current by update_row
+        kidx.clear();
+        km.clear();
+        for (size_t t = 0; t < s_m.size(); t++) {
+            const double m = s_m[t];
+            if (m != 0.0 && !(m < tau2)) {
+                kidx.push_back((int32_t)t);
+                km.push_back(m);
+            }
         }
-        if ((int64_t)buf.size() > lfil) {
-            std::nth_element(buf.begin(), buf.begin() + lfil, buf.end(), by_mag);
-            buf.resize(lfil);
+        clk::time_point tq1 = S.prof ? clk::now() : clk::time_point();
+        if (S.prof) p_kept += (int64_t)kidx.size();
+        if ((int64_t)kidx.size() > lfil) {   // keep the lfil largest (ties: smaller position)
+            if (lfil == 0) {
+                kidx.clear();
+            } else {
+                const double mth = kth_largest(km.data(), km.size(), lfil, mk);
+                int64_t need = lfil;
+                size_t o = 0;
+                ties.clear();
+                for (size_t t = 0; t < km.size(); t++) {
+                    if (km[t] > mth) {
+                        kidx[o++] = kidx[t];
+                        need--;
+                    } else if (km[t] == mth) {
+                        ties.push_back(kidx[t]);
+                    }
+                }
+                if ((int64_t)ties.size() > need) {
+                    std::sort(ties.begin(), ties.end(), [&](int32_t a, int32_t b) { return s_pos[a] < s_pos[b]; });
+                    ties.resize(need);
+                }
+                for (int32_t t : ties) kidx[o++] = t;
+                kidx.resize(o);
+            }
+        }
+        buf.clear();
+        for (int32_t t : kidx) buf.push_back(Ent{s_pos[t], s_col[t], w[s_col[t]], s_m[t]});
+        if (S.prof) {
+            const auto tq2 = clk::now();
+            p_fcand += ns(tq0, tq1);
+            p_fsel += ns(tq1, tq2);
         }
         // pivot: largest kept entry (ties: smaller position) against the diagonal
         int64_t tb = -1;
@@ -289,24 +465,71 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
             di = make_double2(S.drop_tol * std::sqrt(rowmax2), 0.0);
             S.repaired.fetch_add(1, std::memory_order_relaxed);
         }
-        std::sort(buf.begin(), buf.end(), by_pos);
-        {
-            int64_t* c;
+        {   // publish U row i in any order (consumers scatter by column; assembly sorts)
+            int32_t* c;
             double2* v;
             Ua.reserve((int64_t)buf.size() + 1, c, v);
-            c[0] = cnew;
+            c[0] = (int32_t)cnew;
             v[0] = di;
             for (size_t t = 0; t < buf.size(); t++) {
-                c[t + 1] = buf[t].c;
+                c[t + 1] = (int32_t)buf[t].c;
                 v[t + 1] = buf[t].v;
             }
             S.Urow[i] = RowRef{c, v, (int64_t)buf.size() + 1};
+        }
+        S.front.store(i + 1, std::memory_order_release);
+        clk::time_point tp3 = S.prof ? clk::now() : clk::time_point();
+        // off the critical path (later rows need only U rows)
+        // L part: multipliers kept, nonzero, above the threshold; cap; by position
+        buf.clear();
+        for (const Ent& e : lbuf) {
+            const double m = mag2(w[e.c]);   // == e.m: w at eliminated positions is final
+            if (m != 0.0 && !(m < tau2)) buf.push_back(Ent{e.j, e.c, w[e.c], m});
+        }
+        if ((int64_t)buf.size() > lfil) {
+            std::nth_element(buf.begin(), buf.begin() + lfil, buf.end(), by_mag);
+            buf.resize(lfil);
+        }
+        std::sort(buf.begin(), buf.end(), by_pos);
+        {
+            int32_t* c;
+            double2* v;
+            La.reserve((int64_t)buf.size(), c, v);
+            for (size_t t = 0; t < buf.size(); t++) {
+                c[t] = (int32_t)buf[t].j;
+                v[t] = buf[t].v;
+            }
+            S.Lrow[i] = RowRef{c, v, (int64_t)buf.size()};
         }
         for (int64_t c : nz) {
             present[c] = 0;
             w[c] = make_double2(0.0, 0.0);
         }
-        S.front.store(i + 1, std::memory_order_release);
+        Ua.prefault(4096);
+        if (S.prof) p_cand += hi - i;   // span of the U part (positions)
+        clear_bits();
+        drop_snapshot();
+        if (S.prof) {
+            p_post += ns(tp3, clk::now());
+            p_lcand += (int64_t)lbuf.size();
+            p_elim += ns(tp0, tp1);
+            p_wait += ns(tp1, tp2);
+            p_fin += ns(tp2, tp3);
+        }
+    }
+    if (S.prof) {
+        S.t_elim += p_elim - p_spin;
+        S.t_spin += p_spin;
+        S.t_wait += p_wait;
+        S.t_fin += p_fin;
+        S.n_late += p_late;
+        S.t_post += p_post;
+        S.n_cand += p_cand;
+        S.n_lcand += p_lcand;
+        S.t_fcand += p_fcand;
+        S.t_fsel += p_fsel;
+        S.n_kept += p_kept;
+        S.n_snap += p_snap;
     }
 }
 
@@ -315,15 +538,21 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
 void ilut_factor(const HostCSR& A, double drop_tol, double fill_factor, double permtol, int threads, HostCSR& L,
                  HostCSR& U, std::vector<int64_t>& colperm, IlutStats& st) {
     const int64_t n = A.n;
+    SSB_CHECK(n < (int64_t)INT32_MAX, SS_ERR_ARG, "ILUT: n must be < 2^31");
     SSB_CHECK(drop_tol >= 0.0 && fill_factor >= 0.0 && permtol >= 0.0, SS_ERR_ARG,
               "drop_tol, fill_factor and permtol must be >= 0");
-    if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+    // the frontier hand-off spins: never more threads than cores (oversubscribed, a waiting
+    // thread can hold the core the row owner needs -- measured 27x slower at 24 on 16)
+    const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+    if (threads <= 0 || threads > hw) threads = hw;
     threads = (int)std::min<int64_t>(threads, std::max<int64_t>(1, n / 64));
     Shared S(A);
     S.drop_tol = drop_tol;
     S.fill_factor = fill_factor;
     S.permtol = permtol;
     S.n = n;
+    S.prof = std::getenv("SSB_ILUT_PROF") != nullptr;
+    const auto tw0 = std::chrono::steady_clock::now();
     S.perm.reset(new std::atomic<int64_t>[n]);
     S.iperm.reset(new std::atomic<int64_t>[n]);
     for (int64_t c = 0; c < n; c++) {
@@ -337,6 +566,17 @@ void ilut_factor(const HostCSR& A, double drop_tol, double fill_factor, double p
     for (int t = 1; t < threads; t++) pool.emplace_back(worker, std::ref(S), std::ref(La[t]), std::ref(Ua[t]));
     worker(S, La[0], Ua[0]);
     for (auto& th : pool) th.join();
+    if (S.prof) {
+        const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - tw0).count();
+        std::fprintf(stderr,
+                     "ilut prof: n %lld threads %d wall %.3f s | per row (us): elim %.2f spin %.2f "
+                     "wait %.2f finish %.2f (U candidates %.2f cap %.2f) post %.2f | eliminations after F >= i-1 %.2f | "
+                     "U span %.0f kept %.0f, L %.0f | snapshot rows %.3f\n",
+                     (long long)n, threads, wall, S.t_elim * 1e-3 / n, S.t_spin * 1e-3 / n, S.t_wait * 1e-3 / n,
+                     S.t_fin * 1e-3 / n, S.t_fcand * 1e-3 / n, S.t_fsel * 1e-3 / n, S.t_post * 1e-3 / n,
+                     S.n_late * 1e-3 / n, (double)S.n_cand / n, (double)S.n_kept / n, (double)S.n_lcand / n,
+                     (double)S.n_snap / n);
+    }
     const int bad = S.error_row.load();
     SSB_CHECK(bad < 0, SS_ERR_BREAKDOWN, "ILUT: zero pivot at row " + std::to_string(bad) + " with drop_tol = 0");
     colperm.resize(n);
@@ -360,16 +600,26 @@ void ilut_factor(const HostCSR& A, double drop_tol, double fill_factor, double p
         asm_pool.emplace_back([&, t] {
             std::vector<std::pair<int64_t, double2>> tmp;
             for (int64_t i = n * t / nt; i < n * (t + 1) / nt; i++) {
-                std::memcpy(&L.col[L.rowptr[i]], S.Lrow[i].c, S.Lrow[i].len * sizeof(int64_t));
+                for (int64_t q = 0; q < S.Lrow[i].len; q++) L.col[L.rowptr[i] + q] = S.Lrow[i].c[q];
                 std::memcpy(&L.val[L.rowptr[i]], S.Lrow[i].v, S.Lrow[i].len * sizeof(double2));
                 const RowRef& R = S.Urow[i];
                 const int64_t o = U.rowptr[i];
                 if (R.len == 0) continue;
                 U.col[o] = S.iperm[R.c[0]].load(std::memory_order_relaxed);
                 U.val[o] = R.v[0];
+                // published in position order of step i; a later exchange may have moved some
+                bool sorted = true;
+                int64_t prev = -1;
+                for (int64_t q = 1; q < R.len; q++) {
+                    const int64_t pq = S.iperm[R.c[q]].load(std::memory_order_relaxed);
+                    U.col[o + q] = pq;
+                    U.val[o + q] = R.v[q];
+                    sorted &= pq > prev;
+                    prev = pq;
+                }
+                if (sorted) continue;
                 tmp.clear();
-                for (int64_t q = 1; q < R.len; q++)
-                    tmp.emplace_back(S.iperm[R.c[q]].load(std::memory_order_relaxed), R.v[q]);
+                for (int64_t q = 1; q < R.len; q++) tmp.emplace_back(U.col[o + q], U.val[o + q]);
                 std::sort(tmp.begin(), tmp.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
                 for (size_t q = 0; q < tmp.size(); q++) {
                     U.col[o + 1 + q] = tmp[q].first;

@@ -3,6 +3,9 @@
 
 #include <cmath>
 #include <cstdint>
+#include <memory>
+#include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "../../include/ss_b200.h"
@@ -36,11 +39,35 @@ struct DevCSR {
     }
 };
 
+// std::vector whose resize() leaves trivial elements uninitialised: the setup fills its
+// large arrays in parallel (first touch) instead of zeroing GBs on one thread first.
+template <class T>
+struct DefaultInitAlloc : std::allocator<T> {
+    template <class U>
+    struct rebind {
+        using other = DefaultInitAlloc<U>;
+    };
+    DefaultInitAlloc() = default;
+    template <class U>
+    DefaultInitAlloc(const DefaultInitAlloc<U>&) noexcept {}
+    template <class U>
+    void construct(U* p) noexcept(std::is_nothrow_default_constructible<U>::value) {
+        ::new ((void*)p) U;
+    }
+    template <class U, class... Args>
+    void construct(U* p, Args&&... args) {
+        ::new ((void*)p) U(std::forward<Args>(args)...);
+    }
+};
+template <class T>
+using hvec = std::vector<T, DefaultInitAlloc<T>>;
+
 // Host CSR (int64 everywhere) used during setup.
 struct HostCSR {
     int64_t n = 0;
-    std::vector<int64_t> rowptr, col;
-    std::vector<double2> val;
+    std::vector<int64_t> rowptr;
+    hvec<int64_t> col;
+    hvec<double2> val;
     int64_t nnz() const { return (int64_t)col.size(); }
 };
 
@@ -193,7 +220,7 @@ void build_liouvillian(Problem& P);
 void setup_problem(Problem& P, double drop_tol, double fill_factor, double permtol, int threads,
                    ss_setup_info* info);
 // rcm.cpp
-std::vector<int64_t> rcm_order(int64_t n, const std::vector<int64_t>& rowptr, const std::vector<int64_t>& col);
+std::vector<int64_t> rcm_order(int64_t n, const std::vector<int64_t>& rowptr, const hvec<int64_t>& col);
 // ilut.cpp
 struct IlutStats {
     int32_t repaired = 0;

@@ -14,7 +14,7 @@
 
 namespace ssb {
 
-std::vector<int64_t> rcm_order(int64_t n, const std::vector<int64_t>& rowptr, const std::vector<int64_t>& col) {
+std::vector<int64_t> rcm_order(int64_t n, const std::vector<int64_t>& rowptr, const hvec<int64_t>& col) {
     // transpose pattern (counting sort by column)
     std::vector<int64_t> tptr(n + 1, 0), tcol(col.size());
     for (int64_t c : col) tptr[c + 1]++;

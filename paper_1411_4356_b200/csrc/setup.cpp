@@ -7,6 +7,7 @@
 // sec. II: ILUT(d, p).
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <thread>
@@ -129,6 +130,9 @@ int env_int(const char* name, int dflt) {
 void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads, DevBlockTri& T,
                      cudaStream_t s) {
     T.release();
+    const bool prof = std::getenv("SSB_SETUP_PROF") != nullptr;
+    double tpf[8] = {now_ms()};
+    double t_copy = 0;
     const int64_t n = F.n;
     const int64_t nblk = (n + B - 1) / B;
     const int64_t PK = (int64_t)block_trsv_packed(B);
@@ -278,9 +282,10 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
 
     // entries, in block chunks of ~2^26 (bounded host staging); the rows of a chunk of
     // blocks map to contiguous ranges of the far CSR and of list B
+    tpf[1] = now_ms();
     const int64_t kChunk = (int64_t)1 << 26;
-    std::vector<int32_t> fc, bc;
-    std::vector<double2> fv, bv;
+    hvec<int32_t> fc, bc;   // filled in parallel below (no serial zeroing of GBs)
+    hvec<double2> fv, bv;
     auto frow = [&](int64_t k) { return farptr[std::min(n, k * B)]; };
     for (int64_t k0 = 0; k0 < nblk;) {
         int64_t k1 = k0 + 1;
@@ -291,8 +296,13 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
         const int64_t bb = HB.bp[k0 * G], blen = HB.bp[k1 * G] - bb;
         fc.resize(flen);
         fv.resize(flen);
-        bc.assign(blen, 0);
-        bv.assign(blen, make_double2(0.0, 0.0));
+        bc.resize(blen);
+        bv.resize(blen);
+        for (int64_t idx = k0 * G; idx < k1 * G; idx++)   // list padding (multiple of 4 entries)
+            for (int64_t e = HB.bp[idx] + HB.loc[(size_t)idx * NL + B]; e < HB.bp[idx + 1]; e++) {
+                bc[e - bb] = 0;
+                bv[e - bb] = make_double2(0.0, 0.0);
+            }
         parallel_for(r1 - r0, threads, [&](int64_t lo, int64_t hi) {
             for (int64_t ip = r0 + lo; ip < r0 + hi; ip++) {
                 int64_t q0, q1;
@@ -311,6 +321,7 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
                 }
             }
         });
+        const double tc0 = now_ms();
         if (flen) {
             SSB_CUDA(cudaMemcpy(T.fcol + fb, fc.data(), flen * sizeof(int32_t), cudaMemcpyHostToDevice));
             SSB_CUDA(cudaMemcpy(T.fval + fb, fv.data(), flen * sizeof(double2), cudaMemcpyHostToDevice));
@@ -319,8 +330,10 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
             SSB_CUDA(cudaMemcpy(T.nearB.col + bb, bc.data(), blen * sizeof(int32_t), cudaMemcpyHostToDevice));
             SSB_CUDA(cudaMemcpy(T.nearB.val + bb, bv.data(), blen * sizeof(double2), cudaMemcpyHostToDevice));
         }
+        t_copy += now_ms() - tc0;
         k0 = k1;
     }
+    tpf[2] = now_ms();
 
     // dense diagonal blocks -> explicit inverses D_k^{-1}, and Gd_k = D_k^{-1} T_{k,k-d} for
     // d = 1 .. kDense (column-major, G1 first per block), in block chunks
@@ -409,6 +422,9 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
     }
     SSB_CUDA(cudaStreamSynchronize(s));
     block_trsv_prepare(T);
+    if (prof)
+        std::fprintf(stderr, "build_block_tri(%s): layout %.0f ms, entries %.0f ms (copies %.0f), dense blocks %.0f ms\n",
+                     upper ? "U" : "L", tpf[1] - tpf[0], tpf[2] - tpf[1], t_copy, now_ms() - tpf[2]);
 }
 
 // Tuning knobs of the block substitution: rows per block and CTA size.

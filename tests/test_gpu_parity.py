@@ -73,6 +73,26 @@ def test_setup_bit_exact(cuda, name):
     s.close()
 
 
+@pytest.mark.parametrize("name,permtol,threads", [("tiny", 0.5, 0), ("small", 0.5, 1), ("small", 0.5, 5),
+                                                   ("small", 0.01, 3)])
+def test_setup_bit_exact_pivoting(cuda, name, permtol, threads):
+    """Multi-threaded iLUTP (ilut.cpp) with many column exchanges (permtol 0.5) and odd
+    thread counts: factors and permutation bit-identical to the serial oracle."""
+    p = CONFIGS[name].with_(permtol=permtol)
+    s = pb().SteadyState(p).setup(threads=threads)
+    Lt, _, _, _ = lv.constrained_system(p)
+    A = R.permute(Lt, ss.rcm_c(R.symmetrized_pattern(Lt)))
+    F = I.ilutp(A, p.drop_tol, p.fill_factor, p.permtol)
+    if permtol >= 0.5:
+        assert not np.array_equal(F.perm, np.arange(A.shape[0])) and s.setup_info["pivot_swaps"] > 0
+    assert np.array_equal(pb().ss_export_colperm(s.handle), F.perm)
+    for which, (P_, J_, X_) in ((0, (F.Lp, F.Lj, F.Lx)), (1, (F.Up, F.Uj, F.Ux))):
+        gp, gj, gx = pb().ss_export_factors(s.handle, which)
+        assert np.array_equal(gp, P_) and np.array_equal(gj, J_)
+        assert np.array_equal(gx, X_)
+    s.close()
+
+
 @pytest.mark.parametrize("name", ["tiny", "small", "ragged"])
 def test_spmv_and_substitutions(cuda, name):
     torch = cuda
