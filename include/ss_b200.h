@@ -160,6 +160,21 @@ int ss_export_colperm(const ss_problem* h, int64_t* colperm);
 int ss_export_factors(const ss_problem* h, int32_t which, int64_t* rowptr, int64_t* colidx,
                       double* vals);
 
+/* Host-only iLUTP (sec. II; rules R4-R7, R13 of DESIGN.md) of a given CSR
+ * matrix A (n rows, int64 rowptr[n+1] / colidx[nnz] with columns in [0, n) and no
+ * duplicates in a row, complex128 vals[2 nnz]), with the same multi-threaded code and the
+ * same results as ss_setup (bit-identical for any n_threads; n_threads <= 0: all host
+ * cores).  Needs no GPU.  Outputs, caller-allocated: L (strict lower, unit diagonal
+ * implicit) L_rowptr[n+1], L_colidx[L_cap], L_vals[2 L_cap]; U (diagonal first in every
+ * row) U_rowptr[n+1], U_colidx[U_cap], U_vals[2 U_cap]; colperm[n] (A[:, colperm] ~ L U).
+ * Enough room: L_cap = sum_i floor(p nnz(a_i) / 2), U_cap = that + n (rule R5).  Errors:
+ * SS_ERR_ARG (bad arguments, caps too small: the message states the sizes needed),
+ * SS_ERR_BREAKDOWN (zero pivot with drop_tol = 0). */
+int ss_ilutp_host(int64_t n, const int64_t* rowptr, const int64_t* colidx, const double* vals, double drop_tol,
+                  double fill_factor, double permtol, int32_t n_threads, int64_t* L_rowptr, int64_t* L_colidx,
+                  double* L_vals, int64_t L_cap, int64_t* U_rowptr, int64_t* U_colidx, double* U_vals,
+                  int64_t U_cap, int64_t* colperm);
+
 /* y = L~_RCM x  (device pointers, complex128 length n).                           */
 int ss_spmv(ss_problem* h, const void* x_dev, void* y_dev);
 /* y = L^{-1} x (which = 0), y = Pi U^{-1} x (which = 1), y = M^{-1} x = Pi U^{-1} L^{-1} x

@@ -82,6 +82,8 @@ SIGNATURES = [
     ("ss_precond", ctypes.c_int, [P, I32, P, P]),
     ("ss_kernel_launches", ctypes.c_int64, []),
     ("ss_debug_trace_trsv", ctypes.c_int, [P, I32, P, P, P, PI64]),
+    ("ss_ilutp_host", ctypes.c_int, [ctypes.c_int64, P, P, P, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                     I32, P, P, P, ctypes.c_int64, P, P, P, ctypes.c_int64, P]),
 ]
 
 _lib = None
@@ -196,6 +198,25 @@ def ss_export_factors(h, which: int):
     va = np.empty(max(nz, 0), np.complex128)
     _check(load().ss_export_factors(h, int(which), rp.ctypes.data, ci.ctypes.data, va.ctypes.data))
     return rp, ci, va
+
+
+def ss_ilutp_host(rowptr, colidx, vals, drop_tol: float, fill_factor: float, permtol: float, threads: int = 0):
+    """Host-only iLUTP (no GPU) of the CSR matrix (rowptr, colidx, vals): returns
+    ((Lp, Lj, Lx), (Up, Uj, Ux), colperm) exactly as ss_setup computes them."""
+    rp = np.ascontiguousarray(rowptr, np.int64)
+    ci = np.ascontiguousarray(colidx, np.int64)
+    va = np.ascontiguousarray(vals, np.complex128)
+    n = rp.size - 1
+    cap = int(np.sum(np.floor(fill_factor * np.diff(rp) / 2.0)))   # rule R5
+    Lp, Up = np.empty(n + 1, np.int64), np.empty(n + 1, np.int64)
+    Lj, Lx = np.empty(max(cap, 1), np.int64), np.empty(max(cap, 1), np.complex128)
+    Uj, Ux = np.empty(cap + n, np.int64), np.empty(cap + n, np.complex128)
+    cp = np.empty(n, np.int64)
+    _check(load().ss_ilutp_host(n, rp.ctypes.data, ci.ctypes.data, va.ctypes.data, float(drop_tol),
+                                float(fill_factor), float(permtol), int(threads), Lp.ctypes.data, Lj.ctypes.data,
+                                Lx.ctypes.data, max(cap, 1), Up.ctypes.data, Uj.ctypes.data, Ux.ctypes.data,
+                                cap + n, cp.ctypes.data))
+    return (Lp, Lj[:Lp[n]], Lx[:Lp[n]]), (Up, Uj[:Up[n]], Ux[:Up[n]]), cp
 
 
 def ss_spmv(h, x_dev_ptr: int, y_dev_ptr: int):

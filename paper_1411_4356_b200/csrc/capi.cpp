@@ -237,6 +237,49 @@ int ss_export_factors(const ss_problem* h, int32_t which, int64_t* rowptr, int64
     SS_GUARD_END
 }
 
+int ss_ilutp_host(int64_t n, const int64_t* rowptr, const int64_t* colidx, const double* vals, double drop_tol,
+                  double fill_factor, double permtol, int32_t n_threads, int64_t* L_rowptr, int64_t* L_colidx,
+                  double* L_vals, int64_t L_cap, int64_t* U_rowptr, int64_t* U_colidx, double* U_vals,
+                  int64_t U_cap, int64_t* colperm) {
+    SS_GUARD_BEGIN
+    SSB_CHECK(n > 0 && rowptr && colidx && vals && L_rowptr && L_colidx && L_vals && U_rowptr && U_colidx &&
+                  U_vals && colperm && L_cap >= 0 && U_cap >= 0,
+              SS_ERR_ARG, "ss_ilutp_host: NULL or negative argument");
+    SSB_CHECK(rowptr[0] == 0, SS_ERR_ARG, "ss_ilutp_host: rowptr[0] must be 0");
+    HostCSR A;
+    A.n = n;
+    A.rowptr.assign(rowptr, rowptr + n + 1);
+    std::vector<int64_t> mark(n, -1);
+    for (int64_t i = 0; i < n; i++) {
+        SSB_CHECK(rowptr[i + 1] >= rowptr[i], SS_ERR_ARG, "ss_ilutp_host: rowptr must be non-decreasing");
+        for (int64_t q = rowptr[i]; q < rowptr[i + 1]; q++) {
+            const int64_t c = colidx[q];
+            SSB_CHECK(c >= 0 && c < n, SS_ERR_ARG, "ss_ilutp_host: column out of range in row " + std::to_string(i));
+            SSB_CHECK(mark[c] != i, SS_ERR_ARG, "ss_ilutp_host: duplicate column in row " + std::to_string(i));
+            mark[c] = i;
+        }
+    }
+    const int64_t nnz = rowptr[n];
+    A.col.assign(colidx, colidx + nnz);
+    A.val.resize(nnz);
+    std::memcpy(A.val.data(), vals, nnz * sizeof(double2));
+    HostCSR L, U;
+    std::vector<int64_t> cp;
+    IlutStats st;
+    ilut_factor(A, drop_tol, fill_factor, permtol, n_threads, L, U, cp, st);
+    SSB_CHECK(L.nnz() <= L_cap && U.nnz() <= U_cap, SS_ERR_ARG,
+              "ss_ilutp_host: caps too small, need L_cap >= " + std::to_string(L.nnz()) + " and U_cap >= " +
+                  std::to_string(U.nnz()));
+    std::memcpy(L_rowptr, L.rowptr.data(), (n + 1) * sizeof(int64_t));
+    std::memcpy(L_colidx, L.col.data(), L.nnz() * sizeof(int64_t));
+    std::memcpy(L_vals, L.val.data(), L.nnz() * sizeof(double2));
+    std::memcpy(U_rowptr, U.rowptr.data(), (n + 1) * sizeof(int64_t));
+    std::memcpy(U_colidx, U.col.data(), U.nnz() * sizeof(int64_t));
+    std::memcpy(U_vals, U.val.data(), U.nnz() * sizeof(double2));
+    std::memcpy(colperm, cp.data(), n * sizeof(int64_t));
+    SS_GUARD_END
+}
+
 int ss_spmv(ss_problem* h, const void* x_dev, void* y_dev) {
     SS_GUARD_BEGIN
     SSB_CHECK(h && x_dev && y_dev, SS_ERR_ARG, "ss_spmv: NULL argument");
