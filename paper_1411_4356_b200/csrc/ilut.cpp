@@ -192,8 +192,6 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
     nz.reserve(4096);
     buf.reserve(4096);
     lbuf.reserve(4096);
-    auto by_mag = [](const Ent& a, const Ent& b) { return a.m > b.m || (a.m == b.m && a.j < b.j); };
-    auto by_pos = [](const Ent& a, const Ent& b) { return a.j < b.j; };
     const double pt2 = S.permtol * S.permtol;
     uint64_t* bt = bits.data();
     int64_t lo = n, hi = -1;   // range of positions set in this row
@@ -481,16 +479,28 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
         clk::time_point tp3 = S.prof ? clk::now() : clk::time_point();
         // off the critical path (later rows need only U rows)
         // L part: multipliers kept, nonzero, above the threshold; cap; by position
+        // (lbuf is in elimination order = ascending position; w at eliminated positions is
+        // final, so e.v / e.m are the values the serial algorithm caps)
         buf.clear();
-        for (const Ent& e : lbuf) {
-            const double m = mag2(w[e.c]);   // == e.m: w at eliminated positions is final
-            if (m != 0.0 && !(m < tau2)) buf.push_back(Ent{e.j, e.c, w[e.c], m});
+        for (const Ent& e : lbuf)
+            if (e.m != 0.0 && !(e.m < tau2)) buf.push_back(e);
+        if ((int64_t)buf.size() > lfil) {   // lfil largest, ties: smaller position (= earlier)
+            if (lfil == 0) {
+                buf.clear();
+            } else {
+                km.clear();
+                for (const Ent& e : buf) km.push_back(e.m);
+                const double mth = kth_largest(km.data(), km.size(), lfil, mk);
+                int64_t need = lfil;
+                for (const Ent& e : buf) need -= e.m > mth;
+                size_t o = 0;
+                for (size_t t = 0; t < buf.size(); t++) {
+                    const Ent& e = buf[t];
+                    if (e.m > mth || (e.m == mth && need-- > 0)) buf[o++] = e;
+                }
+                buf.resize(o);
+            }
         }
-        if ((int64_t)buf.size() > lfil) {
-            std::nth_element(buf.begin(), buf.begin() + lfil, buf.end(), by_mag);
-            buf.resize(lfil);
-        }
-        std::sort(buf.begin(), buf.end(), by_pos);
         {
             int32_t* c;
             double2* v;
