@@ -118,6 +118,7 @@ struct Shared {
     std::atomic<int64_t> next{0};
     std::atomic<int64_t> front{0};                    // rows < front are published
     std::atomic<int64_t> swap_version{0};             // bumped by every column exchange
+    std::unique_ptr<std::pair<int64_t, int64_t>[]> swap_log;   // exchange v: positions (s, t)
     std::unique_ptr<std::atomic<int64_t>[]> perm;     // position -> original column
     std::unique_ptr<std::atomic<int64_t>[]> iperm;    // original column -> position
     std::vector<RowRef> Lrow, Urow;                   // L: positions; U: original columns
@@ -187,8 +188,21 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
     std::vector<int32_t> sidx(n, -1);   // column -> snapshot index
     std::vector<int64_t> s_pos, s_col;
     std::vector<double> s_m;
-    std::vector<int32_t> kidx, ties;
+    std::vector<int32_t> ties;
     bool snapped = false;
+    // histogram of the kept (not dropped) snapshot magnitudes over binary orders of
+    // magnitude below the row's scale, maintained with s_m: the cap's bucket is known
+    // without a pass
+    constexpr int kHB = 128;
+    uint32_t shist[kHB];
+    double cur_tau2 = 0.0;
+    int cur_base = 0;
+    auto kept = [&](double m) { return m != 0.0 && !(m < cur_tau2); };
+    auto hbin = [&](double m) {
+        uint64_t b;
+        std::memcpy(&b, &m, 8);
+        return std::min(kHB - 1, std::max(0, cur_base - (int)(b >> 52)));
+    };
     nz.reserve(4096);
     buf.reserve(4096);
     lbuf.reserve(4096);
@@ -207,12 +221,15 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
     };
 
     auto take_snapshot = [&](int64_t i) {
+        std::memset(shist, 0, sizeof(shist));
         for (int64_t pp = next_bit(bt, i + 1, hi + 1); pp <= hi; pp = next_bit(bt, pp + 1, hi + 1)) {
             const int64_t c = S.perm[pp].load(std::memory_order_relaxed);
+            const double m = mag2(w[c]);
             sidx[c] = (int32_t)s_col.size();
             s_pos.push_back(pp);
             s_col.push_back(c);
-            s_m.push_back(mag2(w[c]));
+            s_m.push_back(m);
+            if (kept(m)) shist[hbin(m)]++;
         }
         snapped = true;
     };
@@ -257,7 +274,12 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
             wp[c] = t;
             if (SN) {
                 const int32_t si = sidx[c];
-                if (si >= 0) s_m[si] = mag2(t);
+                if (si >= 0) {
+                    const double mo = s_m[si], mn = mag2(t);
+                    if (kept(mo)) shist[hbin(mo)]--;
+                    if (kept(mn)) shist[hbin(mn)]++;
+                    s_m[si] = mn;
+                }
             }
         }
     };
@@ -294,24 +316,33 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
         int64_t cursor = std::min(lo, f0);   // the row's positions < cursor are eliminated (or dropped)
         uint32_t spins = 0;
         const double tau2 = S.drop_tol * S.drop_tol * rowmax2;
+        cur_tau2 = tau2;
+        {
+            uint64_t b;
+            std::memcpy(&b, &rowmax2, 8);
+            cur_base = (int)(b >> 52) + 32;   // bin 0: >= 2^32 rowmax2 (and everything larger)
+        }
 
         // eliminate final positions < min(F, i) in increasing order as F advances.  Positions
         // only change through column exchanges (step s exchanges s and t >= s >= F), which
-        // bump swap_version before the frontier moves on; the bits >= cursor are then
-        // rebuilt from the row's columns (rare).
+        // bump swap_version before the frontier moves on (logging the two positions); the
+        // two bits of every exchange seen are then re-derived.
         for (;;) {
             const int64_t f = S.front.load(std::memory_order_acquire);
             const int64_t ver = S.swap_version.load(std::memory_order_acquire);
             if (ver != my_version) {
                 if (snapped) drop_snapshot();
-                const int64_t keep_lo = lo;
-                clear_bits();
-                for (int64_t c : nz) {
-                    const int64_t pc = S.iperm[c].load(std::memory_order_relaxed);
-                    if (pc >= cursor) setbit(pc);
+                // exchange v swapped positions s and t (both >= the frontier then, so >=
+                // cursor): re-derive those two bits from the columns now there.  This also
+                // repairs a fill bit set from a position read while the exchange was under
+                // way; later exchanges re-derive their own positions when they are seen.
+                for (int64_t v = my_version; v < ver; v++) {
+                    for (const int64_t pp : {S.swap_log[v].first, S.swap_log[v].second}) {
+                        if (pp < cursor) continue;
+                        if (present[S.perm[pp].load(std::memory_order_relaxed)]) setbit(pp);
+                        else bt[pp >> 6] &= ~(1ull << (pp & 63));
+                    }
                 }
-                lo = std::min(lo, keep_lo);   // the clearing range still covers eliminated words
-                hi = std::max(hi, cursor);
                 my_version = ver;
             }
             const int64_t lim = std::min(f, i);
@@ -386,43 +417,39 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
         double2 di = present[cdiag] ? w[cdiag] : make_double2(0.0, 0.0);
         if (S.prof) p_snap += snapped;
         if (!snapped) take_snapshot(i);   // else kept current by update_row
-        kidx.clear();
-        km.clear();
-        for (size_t t = 0; t < s_m.size(); t++) {
-            const double m = s_m[t];
-            if (m != 0.0 && !(m < tau2)) {
-                kidx.push_back((int32_t)t);
-                km.push_back(m);
-            }
-        }
+        int64_t nkept = 0;
+        for (int t = 0; t < kHB; t++) nkept += shist[t];
         clk::time_point tq1 = S.prof ? clk::now() : clk::time_point();
-        if (S.prof) p_kept += (int64_t)kidx.size();
-        if ((int64_t)kidx.size() > lfil) {   // keep the lfil largest (ties: smaller position)
-            if (lfil == 0) {
-                kidx.clear();
-            } else {
-                const double mth = kth_largest(km.data(), km.size(), lfil, mk);
-                int64_t need = lfil;
-                size_t o = 0;
-                ties.clear();
-                for (size_t t = 0; t < km.size(); t++) {
-                    if (km[t] > mth) {
-                        kidx[o++] = kidx[t];
-                        need--;
-                    } else if (km[t] == mth) {
-                        ties.push_back(kidx[t]);
-                    }
-                }
-                if ((int64_t)ties.size() > need) {
-                    std::sort(ties.begin(), ties.end(), [&](int32_t a, int32_t b) { return s_pos[a] < s_pos[b]; });
-                    ties.resize(need);
-                }
-                for (int32_t t : ties) kidx[o++] = t;
-                kidx.resize(o);
-            }
-        }
+        if (S.prof) p_kept += nkept;
         buf.clear();
-        for (int32_t t : kidx) buf.push_back(Ent{s_pos[t], s_col[t], w[s_col[t]], s_m[t]});
+        if (nkept <= lfil) {
+            for (size_t t = 0; t < s_m.size(); t++)
+                if (kept(s_m[t])) buf.push_back(Ent{s_pos[t], s_col[t], w[s_col[t]], s_m[t]});
+        } else if (lfil > 0) {   // keep the lfil largest (ties: smaller position)
+            int hb = 0;
+            int64_t above = 0;
+            while (above + shist[hb] < lfil) above += shist[hb++];
+            mk.clear();
+            for (size_t t = 0; t < s_m.size(); t++) {
+                const double m = s_m[t];
+                if (kept(m) && hbin(m) == hb) mk.push_back(m);
+            }
+            const int64_t r = lfil - above;   // 1 <= r <= shist[hb]
+            std::nth_element(mk.begin(), mk.begin() + (r - 1), mk.end(), std::greater<double>());
+            const double mth = mk[r - 1];
+            ties.clear();
+            for (size_t t = 0; t < s_m.size(); t++) {
+                const double m = s_m[t];
+                if (m > mth && kept(m)) buf.push_back(Ent{s_pos[t], s_col[t], w[s_col[t]], m});
+                else if (m == mth && kept(m)) ties.push_back((int32_t)t);
+            }
+            const int64_t need = lfil - (int64_t)buf.size();
+            if ((int64_t)ties.size() > need) {
+                std::sort(ties.begin(), ties.end(), [&](int32_t x, int32_t y) { return s_pos[x] < s_pos[y]; });
+                ties.resize(need);
+            }
+            for (int32_t t : ties) buf.push_back(Ent{s_pos[t], s_col[t], w[s_col[t]], s_m[t]});
+        }
         if (S.prof) {
             const auto tq2 = clk::now();
             p_fcand += ns(tq0, tq1);
@@ -446,7 +473,9 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
             S.perm[tpos].store(cdiag, std::memory_order_relaxed);
             S.iperm[ct].store(i, std::memory_order_relaxed);
             S.iperm[cdiag].store(tpos, std::memory_order_relaxed);
-            S.swap_version.fetch_add(1, std::memory_order_release);
+            const int64_t v = S.swap_version.load(std::memory_order_relaxed);   // one writer at a time
+            S.swap_log[v] = {i, tpos};
+            S.swap_version.store(v + 1, std::memory_order_release);
             if (old.x != 0.0 || old.y != 0.0) {
                 buf[tb] = Ent{tpos, cdiag, old, mag2(old)};
             } else {
@@ -563,6 +592,7 @@ void ilut_factor(const HostCSR& A, double drop_tol, double fill_factor, double p
     S.n = n;
     S.prof = std::getenv("SSB_ILUT_PROF") != nullptr;
     const auto tw0 = std::chrono::steady_clock::now();
+    S.swap_log.reset(new std::pair<int64_t, int64_t>[n + 1]);   // at most one exchange per row
     S.perm.reset(new std::atomic<int64_t>[n]);
     S.iperm.reset(new std::atomic<int64_t>[n]);
     for (int64_t c = 0; c < n; c++) {

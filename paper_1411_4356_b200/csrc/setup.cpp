@@ -454,10 +454,8 @@ void setup_problem(Problem& P, double drop_tol, double fill_factor, double permt
     const int QMAX = env_int("SSB_TRSV_Q", 32);
     const int QMAX_U = env_int("SSB_TRSV_QU", QMAX);   // (the upper factor's window, if different)
     int64_t levL = 0, levU = 0;
-    std::thread lev([&] {
-        levL = count_levels(P.hL, false);
-        levU = count_levels(P.hU, true);
-    });
+    std::thread lev([&] { levL = count_levels(P.hL, false); });   // diagnostics, off the path
+    std::thread levu([&] { levU = count_levels(P.hU, true); });
     try {
         build_block_tri(P.hL, false, B, QMAX, threads, P.L, s);
         build_block_tri(P.hU, true, B, QMAX_U, threads, P.U, s);
@@ -470,9 +468,11 @@ void setup_problem(Problem& P, double drop_tol, double fill_factor, double permt
         }
     } catch (...) {
         lev.join();
+        levu.join();
         throw;
     }
     lev.join();
+    levu.join();
     P.L.nlev = levL;
     P.U.nlev = levU;
     const double t3 = now_ms();
