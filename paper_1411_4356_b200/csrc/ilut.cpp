@@ -583,7 +583,9 @@ void ilut_factor(const HostCSR& A, double drop_tol, double fill_factor, double p
     // the frontier hand-off spins: never more threads than cores (oversubscribed, a waiting
     // thread can hold the core the row owner needs -- measured 27x slower at 24 on 16)
     const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
-    if (threads <= 0 || threads > hw) threads = hw;
+    const int cap = std::getenv("SSB_ILUT_MAXTHREADS") ? std::atoi(std::getenv("SSB_ILUT_MAXTHREADS")) : hw;
+    if (threads <= 0) threads = hw;
+    if (threads > cap) threads = cap;
     threads = (int)std::min<int64_t>(threads, std::max<int64_t>(1, n / 64));
     Shared S(A);
     S.drop_tol = drop_tol;
