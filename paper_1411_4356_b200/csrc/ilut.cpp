@@ -33,7 +33,9 @@
 // snapshotted while the last kSnapAhead rows are still being finished elsewhere and kept
 // current by the late updates, the cap is a counting selection over binary orders of
 // magnitude, the U row is published in position order as selected, and the L row, the
-// clearing of the work row and the arena page faults are done after publication.
+// clearing of the work row and the arena page faults are done after publication.  Each
+// thread keeps two rows in flight (RowWork): while the row it publishes next waits for the
+// frontier, it eliminates ahead in the next one (SSB_ILUT_ROWS=1: one row).
 // SSB_ILUT_PROF=1 prints the per-row time of each phase.
 #include <algorithm>
 #include <atomic>
@@ -124,6 +126,7 @@ struct Shared {
     std::vector<RowRef> Lrow, Urow;                   // L: positions; U: original columns
     std::atomic<int> error_row{-1};
     std::atomic<int32_t> repaired{0}, swaps{0};
+    int rows_per_thread = 2;                          // SSB_ILUT_ROWS (1 or 2)
     bool prof = false;                                // SSB_ILUT_PROF: per-phase times (stderr)
     std::atomic<int64_t> t_elim{0}, t_spin{0}, t_wait{0}, t_fin{0}, n_late{0}, t_post{0}, n_cand{0}, n_lcand{0},
         t_fcand{0}, t_fsel{0}, n_kept{0}, n_snap{0};
@@ -172,20 +175,30 @@ inline double kth_largest(const double* m, size_t cnt, int64_t k, std::vector<do
     return tmp[r - 1];
 }
 
-void worker(Shared& S, Arena& La, Arena& Ua) {
-    const int64_t n = S.n;
-    std::vector<double2> w(n, make_double2(0.0, 0.0));   // indexed by ORIGINAL column
-    std::vector<uint8_t> present(n, 0);
+using clk = std::chrono::steady_clock;
+inline int64_t ns_between(clk::time_point a, clk::time_point b) {
+    return (int64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(b - a).count();
+}
+
+// One row in factorisation: its work row, position bitmap, U-candidate snapshot and
+// progress.  A thread holds up to two (worker below): the row it will publish next
+// and, while that one waits for the frontier, the next row it claimed.
+struct RowWork {
+    Shared& S;
+    const int64_t n;
+    std::vector<double2> w;        // indexed by ORIGINAL column
+    std::vector<uint8_t> present;
     // the row's columns by POSITION: bit p set = the column at position p is in the row.
     // Positions are eliminated in increasing order by scanning the bits (fill from U row k
     // lies at positions > k), the U part is the bits >= i.
-    std::vector<uint64_t> bits(((size_t)n >> 6) + 2, 0);
+    std::vector<uint64_t> bits;
+    uint64_t* bt;
     std::vector<int64_t> nz;
     std::vector<Ent> lbuf, buf;
     std::vector<double> mk, km;
     // U candidates of the row (positions > i): snapshot taken while the last rows before i are
     // finished by other threads; afterwards only the entries the late U rows touch change
-    std::vector<int32_t> sidx(n, -1);   // column -> snapshot index
+    std::vector<int32_t> sidx;   // column -> snapshot index
     std::vector<int64_t> s_pos, s_col;
     std::vector<double> s_m;
     std::vector<int32_t> ties;
@@ -193,34 +206,45 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
     // histogram of the kept (not dropped) snapshot magnitudes over binary orders of
     // magnitude below the row's scale, maintained with s_m: the cap's bucket is known
     // without a pass
-    constexpr int kHB = 128;
+    static constexpr int kHB = 128;
     uint32_t shist[kHB];
-    double cur_tau2 = 0.0;
+    // the row
+    bool active = false;
+    int64_t i = -1, lfil = 0, cursor = 0, my_version = 0, lo, hi = -1;
+    double rowmax2 = 0.0, tau2 = 0.0;
     int cur_base = 0;
-    auto kept = [&](double m) { return m != 0.0 && !(m < cur_tau2); };
-    auto hbin = [&](double m) {
+    // profile (SSB_ILUT_PROF)
+    clk::time_point tp0;
+    int64_t p_elim = 0, p_late = 0, p_wait = 0, p_fin = 0, p_post = 0, p_cand = 0, p_lcand = 0;
+    int64_t p_fcand = 0, p_fsel = 0, p_kept = 0, p_snap = 0;
+
+    enum { kWorked, kIdle, kReady, kError };
+
+    explicit RowWork(Shared& s)
+        : S(s), n(s.n), w(s.n, make_double2(0.0, 0.0)), present(s.n, 0), bits(((size_t)s.n >> 6) + 2, 0),
+          sidx(s.n, -1), lo(s.n) {
+        bt = bits.data();
+        nz.reserve(4096);
+        buf.reserve(4096);
+        lbuf.reserve(4096);
+    }
+    bool kept(double m) const { return m != 0.0 && !(m < tau2); }
+    int hbin(double m) const {
         uint64_t b;
         std::memcpy(&b, &m, 8);
         return std::min(kHB - 1, std::max(0, cur_base - (int)(b >> 52)));
-    };
-    nz.reserve(4096);
-    buf.reserve(4096);
-    lbuf.reserve(4096);
-    const double pt2 = S.permtol * S.permtol;
-    uint64_t* bt = bits.data();
-    int64_t lo = n, hi = -1;   // range of positions set in this row
-    auto setbit = [&](int64_t p) {
+    }
+    void setbit(int64_t p) {
         bt[p >> 6] |= 1ull << (p & 63);
         lo = std::min(lo, p);
         hi = std::max(hi, p);
-    };
-    auto clear_bits = [&]() {
+    }
+    void clear_bits() {
         if (hi >= lo) std::memset(bt + (lo >> 6), 0, (size_t)((hi >> 6) - (lo >> 6) + 1) * sizeof(uint64_t));
         lo = n;
         hi = -1;
-    };
-
-    auto take_snapshot = [&](int64_t i) {
+    }
+    void take_snapshot() {
         std::memset(shist, 0, sizeof(shist));
         for (int64_t pp = next_bit(bt, i + 1, hi + 1); pp <= hi; pp = next_bit(bt, pp + 1, hi + 1)) {
             const int64_t c = S.perm[pp].load(std::memory_order_relaxed);
@@ -232,19 +256,19 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
             if (kept(m)) shist[hbin(m)]++;
         }
         snapped = true;
-    };
-    auto drop_snapshot = [&]() {
+    }
+    void drop_snapshot() {
         for (int64_t c : s_col) sidx[c] = -1;
         s_pos.clear();
         s_col.clear();
         s_m.clear();
         snapped = false;
-    };
+    }
 
     // w <- w - wk * (U row k), new fill recorded; with a snapshot (SN) also keep the
     // magnitudes of the U candidates (positions > i) current
-    auto update_row = [&](const RowRef& U, double2 wk, int64_t i, auto sn) {
-        constexpr bool SN = decltype(sn)::value;
+    template <bool SN>
+    void update_row(const RowRef& U, double2 wk) {
         const int32_t* __restrict uc = U.c;
         const double2* __restrict uv = U.v;
         double2* __restrict wp = w.data();
@@ -282,28 +306,22 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
                 }
             }
         }
-    };
+    }
 
-    using clk = std::chrono::steady_clock;
-    auto ns = [](clk::time_point a, clk::time_point b) {
-        return (int64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(b - a).count();
-    };
-    int64_t p_elim = 0, p_spin = 0, p_wait = 0, p_fin = 0, p_late = 0, p_post = 0, p_cand = 0, p_lcand = 0;
-    int64_t p_fcand = 0, p_fsel = 0, p_kept = 0, p_snap = 0;
-    for (;;) {
-        const int64_t i = S.next.fetch_add(1, std::memory_order_relaxed);
-        if (i >= n) break;
-        clk::time_point tp0 = S.prof ? clk::now() : clk::time_point();
+    void begin(int64_t row) {
+        active = true;
+        i = row;
+        if (S.prof) tp0 = clk::now();
         const int64_t r0 = S.A.rowptr[i], r1 = S.A.rowptr[i + 1];
-        const int64_t lfil = (int64_t)(S.fill_factor * (double)(r1 - r0) / 2.0);
-        double rowmax2 = 0.0;
+        lfil = (int64_t)(S.fill_factor * (double)(r1 - r0) / 2.0);
+        rowmax2 = 0.0;
         nz.clear();
         lbuf.clear();
         // positions are read after the version: a later exchange is seen as a new version.
         // A position read while an exchange of step s >= f0 is under way may be stale, but
         // then both its old and new value are >= f0, hence cursor <= f0 below.
         const int64_t f0 = S.front.load(std::memory_order_acquire);
-        int64_t my_version = S.swap_version.load(std::memory_order_acquire);
+        my_version = S.swap_version.load(std::memory_order_acquire);
         for (int64_t q = r0; q < r1; q++) {
             const int64_t c = S.A.col[q];
             const double m = mag2(S.A.val[q]);
@@ -313,90 +331,82 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
             nz.push_back(c);
             setbit(S.iperm[c].load(std::memory_order_relaxed));
         }
-        int64_t cursor = std::min(lo, f0);   // the row's positions < cursor are eliminated (or dropped)
-        uint32_t spins = 0;
-        const double tau2 = S.drop_tol * S.drop_tol * rowmax2;
-        cur_tau2 = tau2;
-        {
-            uint64_t b;
-            std::memcpy(&b, &rowmax2, 8);
-            cur_base = (int)(b >> 52) + 32;   // bin 0: >= 2^32 rowmax2 (and everything larger)
-        }
+        cursor = std::min(lo, f0);   // the row's positions < cursor are eliminated (or dropped)
+        tau2 = S.drop_tol * S.drop_tol * rowmax2;
+        uint64_t b;
+        std::memcpy(&b, &rowmax2, 8);
+        cur_base = (int)(b >> 52) + 32;   // bin 0: >= 2^32 rowmax2 (and everything larger)
+    }
 
-        // eliminate final positions < min(F, i) in increasing order as F advances.  Positions
-        // only change through column exchanges (step s exchanges s and t >= s >= F), which
-        // bump swap_version before the frontier moves on (logging the two positions); the
-        // two bits of every exchange seen are then re-derived.
-        for (;;) {
-            const int64_t f = S.front.load(std::memory_order_acquire);
-            const int64_t ver = S.swap_version.load(std::memory_order_acquire);
-            if (ver != my_version) {
-                if (snapped) drop_snapshot();
-                // exchange v swapped positions s and t (both >= the frontier then, so >=
-                // cursor): re-derive those two bits from the columns now there.  This also
-                // repairs a fill bit set from a position read while the exchange was under
-                // way; later exchanges re-derive their own positions when they are seen.
-                for (int64_t v = my_version; v < ver; v++) {
-                    for (const int64_t pp : {S.swap_log[v].first, S.swap_log[v].second}) {
-                        if (pp < cursor) continue;
-                        if (present[S.perm[pp].load(std::memory_order_relaxed)]) setbit(pp);
-                        else bt[pp >> 6] &= ~(1ull << (pp & 63));
-                    }
+    // eliminate final positions < min(F, i) in increasing order as F advances, at most
+    // max_elims of them.  Positions only change through column exchanges (step s exchanges
+    // s and t >= s >= F), which bump swap_version before the frontier moves on (logging the
+    // two positions); the two bits of every exchange seen are then re-derived.
+    int advance(int64_t max_elims) {
+        const int64_t f = S.front.load(std::memory_order_acquire);
+        const int64_t ver = S.swap_version.load(std::memory_order_acquire);
+        if (ver != my_version) {
+            if (snapped) drop_snapshot();
+            // exchange v swapped positions s and t (both >= the frontier then, so >=
+            // cursor): re-derive those two bits from the columns now there.  This also
+            // repairs a fill bit set from a position read while the exchange was under
+            // way; later exchanges re-derive their own positions when they are seen.
+            for (int64_t v = my_version; v < ver; v++) {
+                for (const int64_t pp : {S.swap_log[v].first, S.swap_log[v].second}) {
+                    if (pp < cursor) continue;
+                    if (present[S.perm[pp].load(std::memory_order_relaxed)]) setbit(pp);
+                    else bt[pp >> 6] &= ~(1ull << (pp & 63));
                 }
-                my_version = ver;
             }
-            const int64_t lim = std::min(f, i);
-            int64_t k = next_bit(bt, cursor, lim);
-            if (k >= lim) {
-                cursor = std::max(cursor, lim);
-                if (f >= i) break;
-                if (S.error_row.load(std::memory_order_relaxed) >= 0) break;
-                if (!snapped && f >= i - kSnapAhead) {
-                    take_snapshot(i);
-                    continue;
-                }
-                if (S.prof) {
-                    const auto a = clk::now();
-                    SSB_BACKOFF(spins);
-                    p_spin += ns(a, clk::now());
-                } else {
-                    SSB_BACKOFF(spins);
-                }
+            my_version = ver;
+        }
+        const int64_t lim = std::min(f, i);
+        int64_t k = next_bit(bt, cursor, lim);
+        if (k >= lim) {
+            cursor = std::max(cursor, lim);
+            if (S.error_row.load(std::memory_order_relaxed) >= 0) return kError;
+            if (f >= i) return kReady;
+            if (!snapped && f >= i - kSnapAhead) {
+                take_snapshot();
+                return kWorked;
+            }
+            return kIdle;
+        }
+        const bool late = S.prof && f >= i - 1;
+        const clk::time_point tl = late ? clk::now() : clk::time_point();
+        for (int64_t done = 0; k < lim && done < max_elims; k = next_bit(bt, cursor, lim), done++) {
+            cursor = k + 1;
+            const int64_t ck = S.perm[k].load(std::memory_order_relaxed);
+            const RowRef& U = S.Urow[k];
+            const double2 ukk = U.v[0];
+            const double d = ukk.x * ukk.x + ukk.y * ukk.y;
+            const double2 inv = make_double2(ukk.x / d, -ukk.y / d);
+            const double2 wk0 = w[ck];
+            const double2 wk = make_double2(wk0.x * inv.x - wk0.y * inv.y, wk0.x * inv.y + wk0.y * inv.x);
+            if (mag2(wk) < tau2) {
+                w[ck] = make_double2(0.0, 0.0);
                 continue;
             }
-            const bool late = S.prof && f >= i - 1;
-            const clk::time_point tl = late ? clk::now() : clk::time_point();
-            for (; k < lim; k = next_bit(bt, cursor, lim)) {
-                cursor = k + 1;
-                const int64_t ck = S.perm[k].load(std::memory_order_relaxed);
-                const RowRef& U = S.Urow[k];
-                const double2 ukk = U.v[0];
-                const double d = ukk.x * ukk.x + ukk.y * ukk.y;
-                const double2 inv = make_double2(ukk.x / d, -ukk.y / d);
-                const double2 wk0 = w[ck];
-                const double2 wk = make_double2(wk0.x * inv.x - wk0.y * inv.y, wk0.x * inv.y + wk0.y * inv.x);
-                if (mag2(wk) < tau2) {
-                    w[ck] = make_double2(0.0, 0.0);
-                    continue;
-                }
-                w[ck] = wk;
-                lbuf.push_back(Ent{k, ck, wk, mag2(wk)});
-                if (snapped) {
-                    update_row(U, wk, i, std::true_type{});
-                } else {
-                    update_row(U, wk, i, std::false_type{});
-                }
-            }
-            cursor = std::max(cursor, lim);
-            if (late) p_late += ns(tl, clk::now());
+            w[ck] = wk;
+            lbuf.push_back(Ent{k, ck, wk, mag2(wk)});
+            if (snapped) update_row<true>(U, wk);
+            else update_row<false>(U, wk);
         }
+        if (k >= lim) cursor = std::max(cursor, lim);
+        if (late) p_late += ns_between(tl, clk::now());
+        return kWorked;
+    }
+
+    // F == i: cap, pivot and publish U row i, then (off the critical path) the L row
+    void finish(Arena& La, Arena& Ua, uint32_t& spins) {
+        const double pt2 = S.permtol * S.permtol;
         // wait until every earlier row is published (then nobody else exchanges columns)
-        clk::time_point tp1 = S.prof ? clk::now() : clk::time_point();
+        const clk::time_point tp1 = S.prof ? clk::now() : clk::time_point();
         while (S.front.load(std::memory_order_acquire) < i) {
             if (S.error_row.load(std::memory_order_relaxed) >= 0) break;
             SSB_BACKOFF(spins);
         }
-        clk::time_point tp2 = S.prof ? clk::now() : clk::time_point();
+        const clk::time_point tp2 = S.prof ? clk::now() : clk::time_point();
         if (S.error_row.load(std::memory_order_relaxed) >= 0) {   // drain after a breakdown
             for (int64_t c : nz) {
                 present[c] = 0;
@@ -407,19 +417,20 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
             S.Lrow[i] = RowRef{};
             S.Urow[i] = RowRef{};
             S.front.store(i + 1, std::memory_order_release);
-            continue;
+            active = false;
+            return;
         }
 
         // U part: the row's positions > i (current: no exchange is pending now).  With a
         // snapshot (kept current by update_row since) nothing is re-read.
-        clk::time_point tq0 = S.prof ? clk::now() : clk::time_point();
+        const clk::time_point tq0 = S.prof ? clk::now() : clk::time_point();
         const int64_t cdiag = S.perm[i].load(std::memory_order_relaxed);
         double2 di = present[cdiag] ? w[cdiag] : make_double2(0.0, 0.0);
         if (S.prof) p_snap += snapped;
-        if (!snapped) take_snapshot(i);   // else kept current by update_row
+        if (!snapped) take_snapshot();
         int64_t nkept = 0;
         for (int t = 0; t < kHB; t++) nkept += shist[t];
-        clk::time_point tq1 = S.prof ? clk::now() : clk::time_point();
+        const clk::time_point tq1 = S.prof ? clk::now() : clk::time_point();
         if (S.prof) p_kept += nkept;
         buf.clear();
         if (nkept <= lfil) {
@@ -452,8 +463,8 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
         }
         if (S.prof) {
             const auto tq2 = clk::now();
-            p_fcand += ns(tq0, tq1);
-            p_fsel += ns(tq1, tq2);
+            p_fcand += ns_between(tq0, tq1);
+            p_fsel += ns_between(tq1, tq2);
         }
         // pivot: largest kept entry (ties: smaller position) against the diagonal
         int64_t tb = -1;
@@ -505,7 +516,7 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
             S.Urow[i] = RowRef{c, v, (int64_t)buf.size() + 1};
         }
         S.front.store(i + 1, std::memory_order_release);
-        clk::time_point tp3 = S.prof ? clk::now() : clk::time_point();
+        const clk::time_point tp3 = S.prof ? clk::now() : clk::time_point();
         // off the critical path (later rows need only U rows)
         // L part: multipliers kept, nonzero, above the threshold; cap; by position
         // (lbuf is in elimination order = ascending position; w at eliminated positions is
@@ -549,16 +560,19 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
         clear_bits();
         drop_snapshot();
         if (S.prof) {
-            p_post += ns(tp3, clk::now());
+            p_post += ns_between(tp3, clk::now());
             p_lcand += (int64_t)lbuf.size();
-            p_elim += ns(tp0, tp1);
-            p_wait += ns(tp1, tp2);
-            p_fin += ns(tp2, tp3);
+            p_elim += ns_between(tp0, tp1);
+            p_wait += ns_between(tp1, tp2);
+            p_fin += ns_between(tp2, tp3);
         }
+        active = false;
     }
-    if (S.prof) {
-        S.t_elim += p_elim - p_spin;
-        S.t_spin += p_spin;
+
+    void flush_profile(int64_t spin) {
+        if (!S.prof) return;
+        S.t_elim += p_elim - spin;
+        S.t_spin += spin;
         S.t_wait += p_wait;
         S.t_fin += p_fin;
         S.n_late += p_late;
@@ -570,6 +584,49 @@ void worker(Shared& S, Arena& La, Arena& Ua) {
         S.n_kept += p_kept;
         S.n_snap += p_snap;
     }
+};
+
+// A thread owns the row it will publish next (pri) and, while pri waits for the frontier,
+// works ahead on the next row it claims (sec), a few eliminations at a time so that pri
+// is served as soon as the frontier reaches it.  Rows are claimed in increasing order, so
+// the row at the frontier is always some thread's pri (no deadlock).
+void worker(Shared& S, Arena& La, Arena& Ua) {
+    const int rows_per_thread = S.rows_per_thread;
+    std::unique_ptr<RowWork> A(new RowWork(S)), B(rows_per_thread > 1 ? new RowWork(S) : nullptr);
+    RowWork* pri = A.get();
+    RowWork* sec = B.get();
+    auto claim = [&](RowWork* r) {
+        const int64_t row = S.next.fetch_add(1, std::memory_order_relaxed);
+        if (row >= S.n) return false;
+        r->begin(row);
+        return true;
+    };
+    uint32_t spins = 0;
+    int64_t p_spin = 0;
+    bool more = claim(pri);
+    while (pri->active) {
+        const int st = pri->advance(INT64_MAX);
+        if (st == RowWork::kReady || st == RowWork::kError) {
+            pri->finish(La, Ua, spins);
+            spins = 0;
+            if (sec && sec->active) std::swap(pri, sec);
+            else if (more) more = claim(pri);
+            continue;
+        }
+        if (st == RowWork::kWorked) continue;
+        // pri idle: work ahead on the next row
+        if (sec && !sec->active && more) more = claim(sec);
+        if (sec && sec->active && sec->advance(2) == RowWork::kWorked) continue;
+        if (S.prof) {
+            const auto a = clk::now();
+            SSB_BACKOFF(spins);
+            p_spin += ns_between(a, clk::now());
+        } else {
+            SSB_BACKOFF(spins);
+        }
+    }
+    A->flush_profile(p_spin);
+    if (B) B->flush_profile(0);
 }
 
 }  // namespace
@@ -593,6 +650,7 @@ void ilut_factor(const HostCSR& A, double drop_tol, double fill_factor, double p
     S.permtol = permtol;
     S.n = n;
     S.prof = std::getenv("SSB_ILUT_PROF") != nullptr;
+    if (const char* e = std::getenv("SSB_ILUT_ROWS")) S.rows_per_thread = std::max(1, std::min(2, std::atoi(e)));
     const auto tw0 = std::chrono::steady_clock::now();
     S.swap_log.reset(new std::pair<int64_t, int64_t>[n + 1]);   // at most one exchange per row
     S.perm.reset(new std::atomic<int64_t>[n]);
