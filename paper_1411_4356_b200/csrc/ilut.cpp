@@ -201,12 +201,14 @@ struct RowWork {
     std::vector<int32_t> sidx;   // column -> snapshot index
     std::vector<int64_t> s_pos, s_col;
     std::vector<double> s_m;
+    std::vector<uint8_t> s_bin;   // histogram bin of s_m, kNotKept if dropped
     std::vector<int32_t> ties;
     bool snapped = false;
     // histogram of the kept (not dropped) snapshot magnitudes over binary orders of
     // magnitude below the row's scale, maintained with s_m: the cap's bucket is known
     // without a pass
     static constexpr int kHB = 128;
+    static constexpr uint8_t kNotKept = 255;
     uint32_t shist[kHB];
     // the row
     bool active = false;
@@ -253,7 +255,9 @@ struct RowWork {
             s_pos.push_back(pp);
             s_col.push_back(c);
             s_m.push_back(m);
-            if (kept(m)) shist[hbin(m)]++;
+            const uint8_t bn = kept(m) ? (uint8_t)hbin(m) : kNotKept;
+            s_bin.push_back(bn);
+            if (bn != kNotKept) shist[bn]++;
         }
         snapped = true;
     }
@@ -262,6 +266,7 @@ struct RowWork {
         s_pos.clear();
         s_col.clear();
         s_m.clear();
+        s_bin.clear();
         snapped = false;
     }
 
@@ -287,6 +292,7 @@ struct RowWork {
                     s_pos.push_back(pc);
                     s_col.push_back(c);
                     s_m.push_back(0.0);
+                    s_bin.push_back(kNotKept);
                 }
             }
             const double2 u = uv[q];
@@ -299,10 +305,12 @@ struct RowWork {
             if (SN) {
                 const int32_t si = sidx[c];
                 if (si >= 0) {
-                    const double mo = s_m[si], mn = mag2(t);
-                    if (kept(mo)) shist[hbin(mo)]--;
-                    if (kept(mn)) shist[hbin(mn)]++;
+                    const double mn = mag2(t);
+                    const uint8_t bo = s_bin[si], bn = kept(mn) ? (uint8_t)hbin(mn) : kNotKept;
+                    if (bo != kNotKept) shist[bo]--;
+                    if (bn != kNotKept) shist[bn]++;
                     s_m[si] = mn;
+                    s_bin[si] = bn;
                 }
             }
         }
@@ -433,26 +441,30 @@ struct RowWork {
         const clk::time_point tq1 = S.prof ? clk::now() : clk::time_point();
         if (S.prof) p_kept += nkept;
         buf.clear();
+        const size_t ns = s_m.size();
+        const uint8_t* sb = s_bin.data();
         if (nkept <= lfil) {
-            for (size_t t = 0; t < s_m.size(); t++)
-                if (kept(s_m[t])) buf.push_back(Ent{s_pos[t], s_col[t], w[s_col[t]], s_m[t]});
+            for (size_t t = 0; t < ns; t++)
+                if (sb[t] != kNotKept) buf.push_back(Ent{s_pos[t], s_col[t], w[s_col[t]], s_m[t]});
         } else if (lfil > 0) {   // keep the lfil largest (ties: smaller position)
             int hb = 0;
             int64_t above = 0;
             while (above + shist[hb] < lfil) above += shist[hb++];
             mk.clear();
-            for (size_t t = 0; t < s_m.size(); t++) {
-                const double m = s_m[t];
-                if (kept(m) && hbin(m) == hb) mk.push_back(m);
-            }
+            for (size_t t = 0; t < ns; t++)
+                if (sb[t] == hb) mk.push_back(s_m[t]);
             const int64_t r = lfil - above;   // 1 <= r <= shist[hb]
             std::nth_element(mk.begin(), mk.begin() + (r - 1), mk.end(), std::greater<double>());
             const double mth = mk[r - 1];
             ties.clear();
-            for (size_t t = 0; t < s_m.size(); t++) {
-                const double m = s_m[t];
-                if (m > mth && kept(m)) buf.push_back(Ent{s_pos[t], s_col[t], w[s_col[t]], m});
-                else if (m == mth && kept(m)) ties.push_back((int32_t)t);
+            for (size_t t = 0; t < ns; t++) {   // bins < hb: larger than anything in hb
+                if (sb[t] < hb) {
+                    buf.push_back(Ent{s_pos[t], s_col[t], w[s_col[t]], s_m[t]});
+                } else if (sb[t] == hb) {
+                    const double m = s_m[t];
+                    if (m > mth) buf.push_back(Ent{s_pos[t], s_col[t], w[s_col[t]], m});
+                    else if (m == mth) ties.push_back((int32_t)t);
+                }
             }
             const int64_t need = lfil - (int64_t)buf.size();
             if ((int64_t)ties.size() > need) {
