@@ -127,13 +127,14 @@ struct Shared {
     std::atomic<int> error_row{-1};
     std::atomic<int32_t> repaired{0}, swaps{0};
     int rows_per_thread = 2;                          // SSB_ILUT_ROWS (1 or 2)
+    int64_t snap_ahead = 2;                           // kSnapAhead (SSB_ILUT_SNAP)
     bool prof = false;                                // SSB_ILUT_PROF: per-phase times (stderr)
     std::atomic<int64_t> t_elim{0}, t_spin{0}, t_wait{0}, t_fin{0}, n_late{0}, t_post{0}, n_cand{0}, n_lcand{0},
         t_fcand{0}, t_fsel{0}, n_kept{0}, n_snap{0};
     explicit Shared(const HostCSR& a) : A(a) {}
 };
 
-constexpr int64_t kSnapAhead = 2;   // snapshot the U candidates once F >= i - kSnapAhead
+constexpr int64_t kSnapAhead = 2;   // snapshot the U candidates once F >= i - kSnapAhead (SSB_ILUT_SNAP)
 
 // next set bit of b in [from, lim), else lim
 inline int64_t next_bit(const uint64_t* b, int64_t from, int64_t lim) {
@@ -374,7 +375,7 @@ struct RowWork {
             cursor = std::max(cursor, lim);
             if (S.error_row.load(std::memory_order_relaxed) >= 0) return kError;
             if (f >= i) return kReady;
-            if (!snapped && f >= i - kSnapAhead) {
+            if (!snapped && f >= i - S.snap_ahead) {
                 take_snapshot();
                 return kWorked;
             }
@@ -662,6 +663,7 @@ void ilut_factor(const HostCSR& A, double drop_tol, double fill_factor, double p
     S.permtol = permtol;
     S.n = n;
     S.prof = std::getenv("SSB_ILUT_PROF") != nullptr;
+    if (const char* e = std::getenv("SSB_ILUT_SNAP")) S.snap_ahead = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("SSB_ILUT_ROWS")) S.rows_per_thread = std::max(1, std::min(2, std::atoi(e)));
     const auto tw0 = std::chrono::steady_clock::now();
     S.swap_log.reset(new std::pair<int64_t, int64_t>[n + 1]);   // at most one exchange per row
