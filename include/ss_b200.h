@@ -109,7 +109,8 @@ int ss_build(const ss_params* p, void* cuda_stream, ss_problem** out, ss_build_i
  * symmetric permutation L~_RCM, the iLUTP(drop_tol, fill_factor, permtol) factors
  * L~_RCM Pi ~ L U (sec. II, "dual-threshold and pivoting"; rules R4-R7, R13
  * of DESIGN.md; permtol = 0: no column exchanges = plain ILUT), the block layout of the
- * substitutions and its upload.  n_threads <= 0 -> all host cores.  May be called again
+ * substitutions and its upload.  n_threads <= 0 -> all host cores (more than the host
+ * cores are clamped to that; the factors are the same for any n_threads).  May be called again
  * with other parameters.  Errors: SS_ERR_ARG (negative parameter), SS_ERR_BREAKDOWN
  * (zero pivot with drop_tol = 0). */
 int ss_setup(ss_problem* h, double drop_tol, double fill_factor, double permtol, int32_t n_threads,
