@@ -564,10 +564,9 @@ struct RowWork {
             }
             S.Lrow[i] = RowRef{c, v, (int64_t)buf.size()};
         }
-        for (int64_t c : nz) {
-            present[c] = 0;
-            w[c] = make_double2(0.0, 0.0);
-        }
+        // (w needs no clearing: every read of w is of a present column, and a column becomes
+        // present by an assignment -- the row of A or a zero for new fill)
+        for (int64_t c : nz) present[c] = 0;
         Ua.prefault(4096);
         if (S.prof) p_cand += hi - i;   // span of the U part (positions)
         clear_bits();
