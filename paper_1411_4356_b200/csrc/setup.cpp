@@ -7,6 +7,7 @@
 // sec. II: ILUT(d, p).
 #include <algorithm>
 #include <chrono>
+#include <exception>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -457,8 +458,25 @@ void setup_problem(Problem& P, double drop_tol, double fill_factor, double permt
     std::thread lev([&] { levL = count_levels(P.hL, false); });   // diagnostics, off the path
     std::thread levu([&] { levU = count_levels(P.hU, true); });
     try {
-        build_block_tri(P.hL, false, B, QMAX, threads, P.L, s);
-        build_block_tri(P.hU, true, B, QMAX_U, threads, P.U, s);
+        // the two factors' layouts are independent: build them concurrently (host work of
+        // one overlaps the other's copies)
+        std::exception_ptr errL;
+        std::thread tl([&] {
+            try {
+                SSB_CUDA(cudaSetDevice(P.device));   // the current device is per host thread
+                build_block_tri(P.hL, false, B, QMAX, threads, P.L, s);
+            } catch (...) {
+                errL = std::current_exception();
+            }
+        });
+        try {
+            build_block_tri(P.hU, true, B, QMAX_U, threads, P.U, s);
+        } catch (...) {
+            tl.join();
+            throw;
+        }
+        tl.join();
+        if (errL) std::rethrow_exception(errL);
         bool identity = true;
         for (int64_t q = 0; q < P.n && identity; q++) identity = P.colperm[q] == q;
         if (!identity) {   // ILUTP exchanged columns: the U substitution scatters x = Pi y
