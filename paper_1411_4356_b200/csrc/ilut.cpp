@@ -352,6 +352,8 @@ struct RowWork {
     // s and t >= s >= F), which bump swap_version before the frontier moves on (logging the
     // two positions); the two bits of every exchange seen are then re-derived.
     int advance(int64_t max_elims) {
+        // after a breakdown some rows are drained unpublished: never eliminate against them
+        if (S.error_row.load(std::memory_order_acquire) >= 0) return kError;
         const int64_t f = S.front.load(std::memory_order_acquire);
         const int64_t ver = S.swap_version.load(std::memory_order_acquire);
         if (ver != my_version) {
@@ -423,9 +425,8 @@ struct RowWork {
             }
             clear_bits();
             drop_snapshot();
-            S.Lrow[i] = RowRef{};
-            S.Urow[i] = RowRef{};
-            S.front.store(i + 1, std::memory_order_release);
+            // nothing is published (no null rows, no frontier move): every waiter and every
+            // advance() leaves on error_row
             active = false;
             return;
         }
@@ -652,7 +653,7 @@ void ilut_factor(const HostCSR& A, double drop_tol, double fill_factor, double p
     // the frontier hand-off spins: never more threads than cores (oversubscribed, a waiting
     // thread can hold the core the row owner needs -- measured 27x slower at 24 on 16)
     const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
-    const int cap = std::getenv("SSB_ILUT_MAXTHREADS") ? std::atoi(std::getenv("SSB_ILUT_MAXTHREADS")) : hw;
+    const int cap = std::getenv("SSB_ILUT_MAXTHREADS") ? std::max(1, std::atoi(std::getenv("SSB_ILUT_MAXTHREADS"))) : hw;
     if (threads <= 0) threads = hw;
     if (threads > cap) threads = cap;
     threads = (int)std::min<int64_t>(threads, std::max<int64_t>(1, n / 64));

@@ -121,3 +121,18 @@ def test_errors():
         Z = sp.csr_matrix((np.ones(2, np.complex128), [0, 2], [0, 1, 1, 2]), shape=(3, 3))
         m.ss_ilutp_host(Z.indptr, Z.indices, Z.data, 0.0, 10, 0.0)
     assert e.value.code == 4
+
+
+@pytest.mark.parametrize("threads", [1, 8])
+def test_breakdown_with_later_rows_referencing_drained_rows(threads):
+    """d = 0 and a zero pivot at row 1 (rows 0 and 1 equal); rows 2, 3 reference the
+    rows before them.  The oracle reports the zero pivot; the threaded code must return
+    SS_ERR_BREAKDOWN (never eliminate against a row drained after the breakdown)."""
+    m = pb()
+    A = sp.csr_matrix(np.array([[1, 1, 0, 0], [1, 1, 0, 0], [0, 1, 1, 0], [0, 0, 1, 1]], np.complex128))
+    with pytest.raises(RuntimeError, match="zero pivot at row 1"):
+        I.ilutp(A, 0.0, 10, 0.0)
+    for _ in range(5):
+        with pytest.raises(m.SSError) as e:
+            m.ss_ilutp_host(A.indptr, A.indices, A.data, 0.0, 10, 0.0, threads=threads)
+        assert e.value.code == 4
