@@ -33,6 +33,8 @@ class IluFactors:
     Uj: np.ndarray
     Ux: np.ndarray
     perm: np.ndarray | None = None   # ILUTP column permutation: A[:, perm] ~ L U (None: identity)
+    columns: bool = False            # True: the factors of A^T (column-oriented iLUTP, R16):
+                                     #   A^T[:, perm] ~ L U, i.e. A ~ Pi U^T L^T
 
     @property
     def nnz(self) -> int:
@@ -122,6 +124,23 @@ def ilutp(A, drop_tol: float, fill_factor: float, permtol: float) -> IluFactors:
     perm = np.ctypeslib.as_array(Pm, (n,)).copy()
     lib.oracle_free(ctypes.cast(Pm, ctypes.c_void_p))
     return IluFactors(n, lp, lj, lx, up, uj, ux, perm)
+
+
+def ilutp_columns(A, drop_tol: float, fill_factor: float, permtol: float) -> IluFactors:
+    """Column-oriented iLUTP (reading R16 of DESIGN.md): the factorisation works on the
+    columns of A -- each column's fill is dropped against d times the infinity norm of
+    that column of A, its L and U parts are capped at floor(p nnz(A[:, j]) / 2), and the
+    pivot is exchanged along the column (rows) -- which is exactly the row-wise iLUTP
+    above applied to A^T.  This is the orientation of SuperLU's ILU ("the
+    SuperLU solver from SciPy", which the paper's iLUTP is).
+
+    With A^T Pi = L U (perm: A^T[:, perm] = L U):  Pi^T A = U^T L^T, so
+    M = Pi U^T L^T  and  M^{-1} v = L^{-T} U^{-T} (Pi^T v),  (Pi^T v)[j] = v[perm[j]].
+    """
+    A = sp.csr_matrix(A)
+    F = ilutp(sp.csr_matrix(A.T), drop_tol, fill_factor, permtol)
+    F.columns = True
+    return F
 
 
 def condest(F: IluFactors) -> float:

@@ -5,7 +5,8 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 Pipeline (sec. II-IV):
   build L~, rhs          Eq. (5)                         oracle.liouvillian
   RCM of L~ + L~^T       sec. III, PAPER.md:98            oracle.rcm / rcm_ref.c
-  iLUTP of L~_RCM        sec. II, PAPER.md:94             oracle.ilut (ilutp)
+  iLUTP of L~_RCM        sec. II, PAPER.md:94, :119       oracle.ilut (ilutp_columns: the
+                         column-oriented iLUTP of SuperLU, R16; ilutp: row-wise)
   GMRES(m), left prec.   sec. IV, Eq. (8)    oracle.gmres
   un-permute, unvec      Eq. (4) column stacking
 and the reference answer of the linear system itself:
@@ -30,7 +31,7 @@ import scipy.sparse.linalg as sla
 from . import liouvillian as lv
 from . import rcm as rcm_py
 from . import _clib
-from .ilut import ilutp, IluFactors
+from .ilut import ilutp, ilutp_columns, IluFactors
 from .trisolve import apply_preconditioner
 from .gmres import gmres, GmresResult
 
@@ -76,14 +77,24 @@ class IterativeResult:
     times: dict
 
 
-def solve_iterative(p, use_c_rcm: bool = True) -> IterativeResult:
+def factor(A: sp.csr_matrix, p, orientation: str = "columns") -> IluFactors:
+    """The iLUTP(d, p, permtol) of L~_RCM: column-oriented (the reading R16, default) or
+    row-oriented (R13; kept for the study of DESIGN.md R16)."""
+    if orientation == "columns":
+        return ilutp_columns(A, p.drop_tol, p.fill_factor, p.permtol)
+    if orientation == "rows":
+        return ilutp(A, p.drop_tol, p.fill_factor, p.permtol)
+    raise ValueError(f"orientation must be 'columns' or 'rows', not {orientation!r}")
+
+
+def solve_iterative(p, use_c_rcm: bool = True, orientation: str = "columns") -> IterativeResult:
     t0 = time.perf_counter()
     Lt, rhs, w, L = lv.constrained_system(p)
     t1 = time.perf_counter()
     perm = order(Lt, use_c=use_c_rcm)
     A = rcm_py.permute(Lt, perm)
     t2 = time.perf_counter()
-    F = ilutp(A, p.drop_tol, p.fill_factor, p.permtol)
+    F = factor(A, p, orientation)
     t3 = time.perf_counter()
     res = gmres(lambda v: A @ v, lambda v: apply_preconditioner(F, v), rhs[perm], p.restart, p.tol,
                 p.max_iter)

@@ -208,3 +208,99 @@ def test_ilutp_hand_worked_exchange():
     assert np.allclose(U, [[4, 1, 0], [0, 1.75, 1], [0, 0, 22 / 7]], rtol=0, atol=1e-15)
     Lm = F.L().toarray()
     assert np.allclose(Lm, [[0, 0, 0], [0.25, 0, 0], [0.25, -1 / 7, 0]], rtol=0, atol=1e-15)
+
+
+def perm_matrix(perm):
+    """Pi with B Pi = B[:, perm]: Pi[perm[j], j] = 1 (built from the definition)."""
+    n = len(perm)
+    P = np.zeros((n, n))
+    P[perm, np.arange(n)] = 1.0
+    return P
+
+
+def cycle_lengths(perm):
+    seen, out = set(), []
+    for s in range(len(perm)):
+        if s in seen:
+            continue
+        k, c = s, 0
+        while k not in seen:
+            seen.add(k)
+            k = perm[k]
+            c += 1
+        out.append(c)
+    return out
+
+
+def small_diagonal(n, seed):
+    """Dense-ish complex matrix with a tiny diagonal: iLUTP must exchange at most rows,
+    and the exchanges compose into permutation cycles longer than 2."""
+    rng = np.random.default_rng(seed)
+    M = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    M[rng.random((n, n)) < 0.4] = 0.0
+    np.fill_diagonal(M, 1e-3 * (1 + rng.random(n)))
+    A = sp.csr_matrix(M)
+    A.sort_indices()
+    return A
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_row_ilutp_unpivot_with_long_cycles(seed):
+    """Pins the Pi of M^{-1} = Pi U^{-1} L^{-1} (row-wise iLUTP, R13): with d = 0 and
+    unbounded fill the factors are complete, so M^{-1} (A x) = x for every x -- only if
+    Pi (not Pi^{-1}) is applied, which differs once perm has a cycle longer than 2."""
+    A = small_diagonal(24, seed)
+    F = I.ilutp(A, 0.0, 1e9, 0.5)
+    assert max(cycle_lengths(F.perm)) > 2
+    Ad = A.toarray()
+    Lm = (F.L() + sp.identity(24)).toarray()
+    assert np.abs(Lm @ F.U().toarray() - Ad @ perm_matrix(F.perm)).max() <= 1e-9 * np.abs(Ad).max()
+    x = np.random.default_rng(seed + 7).standard_normal(24) + 1j
+    for loops in (True, False):
+        assert np.abs(T.apply_preconditioner(F, Ad @ x, small_loops=loops) - x).max() <= 1e-9 * np.abs(x).max()
+    y = T.backward(F, T.forward(F, Ad @ x))
+    right = np.empty(24, complex)
+    right[F.perm] = y                    # x = Pi y: x[perm[p]] = y[p]
+    assert np.abs(right - x).max() <= 1e-9 * np.abs(x).max()
+    wrong = y[F.perm]                    # Pi^{-1} y instead
+    assert np.abs(wrong - x).max() > 1e-3
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_column_ilutp_complete_with_long_cycles(seed):
+    """Column-oriented iLUTP (R16): A^T Pi = L U, hence A = Pi U^T L^T; with d = 0 and
+    unbounded fill this is exact, so M^{-1} (A x) = L^{-T} U^{-T} Pi^T A x = x (textbook
+    column-sweep loops and library triangular solves), and the pivot rule holds along the
+    COLUMNS of A (every pivot >= permtol times the largest entry of its column of the
+    lower factor)."""
+    A = small_diagonal(24, seed)
+    F = I.ilutp_columns(A, 0.0, 1e9, 0.5)
+    assert F.columns and max(cycle_lengths(F.perm)) > 2
+    Ad = A.toarray()
+    Lm = (F.L() + sp.identity(24)).toarray()
+    U = F.U().toarray()
+    assert np.abs(perm_matrix(F.perm) @ U.T @ Lm.T - Ad).max() <= 1e-9 * np.abs(Ad).max()
+    lower = U.T   # the factor of A that carries the pivots
+    for j in range(24):
+        assert abs(lower[j, j]) >= 0.5 * np.abs(lower[j:, j]).max() * (1 - 1e-12)
+    x = np.random.default_rng(seed + 9).standard_normal(24) + 1j
+    for loops in (True, False):
+        assert np.abs(T.apply_preconditioner(F, Ad @ x, small_loops=loops) - x).max() <= 1e-9 * np.abs(x).max()
+
+
+def test_column_ilutp_hand_worked_drop():
+    """Column orientation, by hand: A = [[4, 1, 0.001], [1, 4, 1], [0, 1, 4]], d = 0.01.
+    Column 0 = (4, 1, 0): pivot 4, no exchange (permtol 0.01).  Column 1 = (1, 4, 1): its
+    entry above the diagonal gives the multiplier 1/4 (kept), then 4 - 1/4 = 3.75.
+    Column 2 = (0.001, 1, 4), threshold 0.01 * ||A[:, 2]||_inf = 0.04: the multiplier
+    0.001/4 = 2.5e-4 is dropped (no update), 1/3.75 is kept, pivot 4 - 1/3.75.
+    (The multipliers land in the unit UPPER factor of A: the column orientation.)
+    """
+    A = sp.csr_matrix(np.array([[4, 1, 0.001], [1, 4, 1], [0, 1, 4]], dtype=complex))
+    F = I.ilutp_columns(A, 0.01, 100, 0.01)
+    assert F.perm.tolist() == [0, 1, 2]
+    u11 = 4 - 0.25
+    lower = F.U().toarray().T            # lower factor of A, pivots on the diagonal
+    upper = (F.L() + sp.identity(3)).toarray().T   # unit upper factor of A
+    assert np.allclose(upper, [[1, 0.25, 0], [0, 1, 1 / u11], [0, 0, 1]], rtol=0, atol=1e-15)
+    assert np.allclose(lower, [[4, 0, 0], [1, u11, 0], [0, 1, 4 - 1 / u11]], rtol=0, atol=1e-15)
