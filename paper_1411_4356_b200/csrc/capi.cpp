@@ -25,8 +25,10 @@ void Problem::release() {
     U.release();
     K.release();
     cudaFree(d_perm);
+    cudaFree(d_rowperm);
     cudaFree(rho);
     d_perm = nullptr;
+    d_rowperm = nullptr;
     rho = nullptr;
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -120,12 +122,9 @@ int ss_solve(ss_problem* h, int32_t restart, double tol, int32_t max_iter, ss_so
     Problem& P = h->P;
     SSB_CHECK(P.have_setup, SS_ERR_STATE, "ss_solve before ss_setup");
     ensure_krylov(P, restart);
-    // b_RCM[k] = b[perm[k]], b = (w, 0, ..., 0): w at the position of old index 0
-    int64_t pos0 = -1;
-    for (int64_t k = 0; k < P.n; k++)
-        if (P.perm[k] == 0) { pos0 = k; break; }
+    // b' = b in the row order of A' (b = (w, 0, ..., 0): w in row rhs_pos, found at setup)
     SSB_CUDA(cudaMemsetAsync(P.K.b, 0, P.n * sizeof(double2), P.stream));
-    SSB_CUDA(cudaMemcpyAsync(P.K.b + pos0, &P.w, sizeof(double2), cudaMemcpyHostToDevice, P.stream));
+    SSB_CUDA(cudaMemcpyAsync(P.K.b + P.rhs_pos, &P.w, sizeof(double2), cudaMemcpyHostToDevice, P.stream));
     ss_solve_info loc{};
     gmres_solve(P, P.K.b, restart, tol, max_iter, &loc);
     finish_solution(P, &loc);
@@ -142,14 +141,14 @@ int ss_solve_host(ss_problem* h, const double* rhs_host, double* x_host, int32_t
     ensure_krylov(P, restart);
     const int64_t n = P.n;
     cudaStream_t s = P.stream;
-    // natural-order rhs -> device (scratch K.r) -> RCM order into K.b
+    // natural-order rhs -> device (scratch K.r) -> the row order of A' into K.b
     if (rhs_host) {
         SSB_CUDA(cudaMemcpyAsync(P.K.r, rhs_host, n * sizeof(double2), cudaMemcpyHostToDevice, s));
     } else {
         SSB_CUDA(cudaMemsetAsync(P.K.r, 0, n * sizeof(double2), s));
         SSB_CUDA(cudaMemcpyAsync(P.K.r, &P.w, sizeof(double2), cudaMemcpyHostToDevice, s));
     }
-    gather_perm(P.K.r, P.d_perm, n, P.K.b, s);
+    gather_perm(P.K.r, P.d_rowperm, n, P.K.b, s);
     ss_solve_info loc{};
     gmres_solve(P, P.K.b, restart, tol, max_iter, &loc);
     finish_solution(P, &loc);   // also scatters x to natural order (in rho, then normalised)

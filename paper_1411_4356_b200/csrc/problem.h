@@ -195,14 +195,17 @@ struct Problem {
     double2 w{0.0, 0.0};
 
     DevCSR nat;                 // L~ natural order
-    DevCSR A;                   // L~_RCM
-    std::vector<int64_t> perm;  // new -> old
+    DevCSR A;                   // A' = Pi^T L~_RCM: L~_RCM with its rows in iLUTP pivot order (R16)
+    std::vector<int64_t> perm;  // new -> old (RCM; the columns of A', the index of x)
+    std::vector<int64_t> rowperm;   // row j of A' is row rowperm[j] of L~ (natural index)
+    int64_t rhs_pos = -1;       // the row of A' holding w of b = (w, 0, ...)
     int64_t* d_perm = nullptr;
+    int64_t* d_rowperm = nullptr;
     bool have_setup = false;
 
-    HostCSR hL, hU;             // host copies of the factors (export / tests)
-    std::vector<int64_t> colperm;   // ILUTP column permutation (position -> column of L~_RCM)
-    DevBlockTri L, U;
+    HostCSR hL, hU;             // iLUTP of L~_RCM^T (export / tests): L~_RCM^T[:, colperm] ~ hL hU
+    std::vector<int64_t> colperm;   // its column permutation = the row order of A'
+    DevBlockTri L, U;           // the substitutions: L <- U'^T (lower, pivots), U <- L'^T (unit upper)
     int64_t bw_nat = 0, bw_rcm = 0;
 
     Krylov K;

@@ -85,6 +85,45 @@ HostCSR permute(const HostCSR& A, const std::vector<int64_t>& perm) {
     return B;
 }
 
+// B = A^T, columns ascending in every row of B.  skip_first: leave out the first stored
+// entry of every row of A (the diagonal of a diagonal-first U factor).
+HostCSR transpose(const HostCSR& A, bool skip_first) {
+    const int64_t n = A.n;
+    HostCSR B;
+    B.n = n;
+    B.rowptr.assign(n + 1, 0);
+    for (int64_t i = 0; i < n; i++)
+        for (int64_t q = A.rowptr[i] + (skip_first ? 1 : 0); q < A.rowptr[i + 1]; q++) B.rowptr[A.col[q] + 1]++;
+    for (int64_t j = 0; j < n; j++) B.rowptr[j + 1] += B.rowptr[j];
+    B.col.resize(B.rowptr[n]);
+    B.val.resize(B.rowptr[n]);
+    std::vector<int64_t> next(B.rowptr.begin(), B.rowptr.end() - 1);
+    for (int64_t i = 0; i < n; i++)
+        for (int64_t q = A.rowptr[i] + (skip_first ? 1 : 0); q < A.rowptr[i + 1]; q++) {
+            const int64_t t = next[A.col[q]]++;
+            B.col[t] = i;
+            B.val[t] = A.val[q];
+        }
+    return B;
+}
+
+// B[j][*] = A[rows[j]][*] (rows reordered, columns unchanged)
+HostCSR permute_rows(const HostCSR& A, const std::vector<int64_t>& rows) {
+    const int64_t n = A.n;
+    HostCSR B;
+    B.n = n;
+    B.rowptr.assign(n + 1, 0);
+    for (int64_t j = 0; j < n; j++) B.rowptr[j + 1] = B.rowptr[j] + (A.rowptr[rows[j] + 1] - A.rowptr[rows[j]]);
+    B.col.resize(A.nnz());
+    B.val.resize(A.nnz());
+    for (int64_t j = 0; j < n; j++) {
+        const int64_t o = rows[j];
+        std::copy(A.col.begin() + A.rowptr[o], A.col.begin() + A.rowptr[o + 1], B.col.begin() + B.rowptr[j]);
+        std::copy(A.val.begin() + A.rowptr[o], A.val.begin() + A.rowptr[o + 1], B.val.begin() + B.rowptr[j]);
+    }
+    return B;
+}
+
 template <class Fn>
 void parallel_for(int64_t n, int threads, Fn fn, int64_t grain = 1024) {
     threads = (int)std::max<int64_t>(1, std::min<int64_t>(threads, n / grain + 1));
@@ -98,13 +137,13 @@ void parallel_for(int64_t n, int threads, Fn fn, int64_t grain = 1024) {
 
 // Row-level dependency levels of the substitution (diagnostic: the length of the
 // chain a row-level schedule would walk).
-int64_t count_levels(const HostCSR& F, bool upper) {
+int64_t count_levels(const HostCSR& F, bool upper) {   // F: strict triangle
     const int64_t n = F.n;
     std::vector<int32_t> lev(n, 0);
     int32_t maxl = 0;
     auto row = [&](int64_t i) {
         int32_t l = 0;
-        for (int64_t q = F.rowptr[i] + (upper ? 1 : 0); q < F.rowptr[i + 1]; q++) l = std::max(l, lev[F.col[q]] + 1);
+        for (int64_t q = F.rowptr[i]; q < F.rowptr[i + 1]; q++) l = std::max(l, lev[F.col[q]] + 1);
         lev[i] = l;
         maxl = std::max(maxl, l);
     };
@@ -115,8 +154,9 @@ int64_t count_levels(const HostCSR& F, bool upper) {
     return n ? (int64_t)maxl + 1 : 0;
 }
 
-// Block layout of one ILU factor for trsv.cu.  Kernel index space: L as is; U reversed
-// (i' = n-1-i), which turns the upper factor into a lower one.  Row i' of block k splits
+// Block layout of one triangular factor for trsv.cu, given as its STRICT triangle F (CSR,
+// columns ascending) and its diagonal (diag = nullptr: unit).  Kernel index space: a
+// lower factor as is; an upper one reversed (i' = n-1-i), which turns it into a lower one.  Row i' of block k splits
 // its strict entries (ascending kernel column) into "far" (source block <= k-Q), "near"
 // (source blocks k-Q+1 .. k-1) and in-block.  Far entries form a CSR; the near entries
 // of a block form one list (rows in order, start padded to 4 entries for TMA, row
@@ -128,8 +168,8 @@ int env_int(const char* name, int dflt) {
     return e ? std::atoi(e) : dflt;
 }
 
-void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads, DevBlockTri& T,
-                     cudaStream_t s) {
+void build_block_tri(const HostCSR& F, const double2* diag, bool upper, int B, int q_max, int threads,
+                     DevBlockTri& T, cudaStream_t s) {
     T.release();
     const bool prof = std::getenv("SSB_SETUP_PROF") != nullptr;
     double tpf[8] = {now_ms()};
@@ -145,7 +185,7 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
     // the reversed strict part of row n-1-ip.
     auto row_range = [&](int64_t ip, int64_t& q0, int64_t& q1) {
         const int64_t i = upper ? n - 1 - ip : ip;
-        q0 = F.rowptr[i] + (upper ? 1 : 0);
+        q0 = F.rowptr[i];
         q1 = F.rowptr[i + 1];
     };
     auto kcol = [&](int64_t q) -> int64_t { return upper ? n - 1 - F.col[q] : F.col[q]; };
@@ -255,7 +295,7 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
     T.nnz_far = nf;
     T.nnz_near = 0;
     for (int64_t i = 0; i < n; i++) T.nnz_near += nin[i] - cnt[i];
-    T.nnz_strict = F.nnz() - (upper ? n : 0);
+    T.nnz_strict = F.nnz();
 
     auto upload_near = [&](const NearHost& H, int64_t total, NearDev& D) {
         SSB_CUDA(cudaMalloc(&D.bp, H.bp.size() * sizeof(int64_t)));
@@ -362,7 +402,7 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
                         D[(size_t)r * B + (kcol(q) - kb)] = F.val[q];
                     }
                     const int64_t i = upper ? n - 1 - ip : ip;
-                    D[(size_t)r * B + r] = upper ? F.val[F.rowptr[i]] : make_double2(1.0, 0.0);
+                    D[(size_t)r * B + r] = diag ? diag[i] : make_double2(1.0, 0.0);
                 }
                 for (int r = 0; r < B; r++) {
                     const double2 d = D[(size_t)r * B + r];
@@ -435,6 +475,7 @@ void build_block_tri(const HostCSR& F, bool upper, int B, int q_max, int threads
 void setup_problem(Problem& P, double drop_tol, double fill_factor, double permtol, int threads,
                    ss_setup_info* info) {
     cudaStream_t s = P.stream;
+    SSB_CUDA(cudaSetDevice(P.device));   // every allocation below (and the helper thread's) on P's device
     P.have_setup = false;
     const double t0 = now_ms();
     HostCSR nat;
@@ -444,19 +485,48 @@ void setup_problem(Problem& P, double drop_tol, double fill_factor, double permt
     HostCSR A = permute(nat, P.perm);
     P.bw_rcm = bandwidth(A);
     const double t1 = now_ms();
+    // column-oriented iLUTP (R16): the row-wise iLUTP of L~_RCM^T,
+    //   L~_RCM^T Pi = L' U'   <=>   Pi^T L~_RCM = U'^T L'^T
     IlutStats st;
-    ilut_factor(A, drop_tol, fill_factor, permtol, threads, P.hL, P.hU, P.colperm, st);
+    {
+        const HostCSR At = transpose(A, false);
+        ilut_factor(At, drop_tol, fill_factor, permtol, threads, P.hL, P.hU, P.colperm, st);
+    }
     const double t2 = now_ms();
-    upload(A, P.A, s);
-    if (!P.d_perm) SSB_CUDA(cudaMalloc(&P.d_perm, P.n * sizeof(int64_t)));
-    SSB_CUDA(cudaMemcpyAsync(P.d_perm, P.perm.data(), P.n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    // the hot path solves the row-permuted system A' x = b', A' = Pi^T L~_RCM (row j of A' is
+    // row colperm[j] of L~_RCM), preconditioned by M'^{-1} = L'^{-T} U'^{-T}: the same Krylov
+    // space as M^{-1} L~_RCM with M = Pi U'^T L'^T, and no permutation left in the loop
+    const int64_t n = P.n;
+    {
+        const HostCSR Ar = permute_rows(A, P.colperm);
+        upload(Ar, P.A, s);
+    }
+    P.rowperm.resize(n);
+    P.rhs_pos = -1;
+    for (int64_t j = 0; j < n; j++) {
+        P.rowperm[j] = P.perm[P.colperm[j]];   // natural index of row j of A'
+        if (P.rowperm[j] == 0) P.rhs_pos = j;  // b = (w, 0, ...): w sits in row 0 of L~
+    }
+    if (!P.d_perm) SSB_CUDA(cudaMalloc(&P.d_perm, n * sizeof(int64_t)));
+    if (!P.d_rowperm) SSB_CUDA(cudaMalloc(&P.d_rowperm, n * sizeof(int64_t)));
+    SSB_CUDA(cudaMemcpyAsync(P.d_perm, P.perm.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    SSB_CUDA(cudaMemcpyAsync(P.d_rowperm, P.rowperm.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
     if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
     const int B = env_int("SSB_TRSV_B", 32);
     const int QMAX = env_int("SSB_TRSV_Q", 32);
     const int QMAX_U = env_int("SSB_TRSV_QU", QMAX);   // (the upper factor's window, if different)
+    // the two substitutions: first U'^T (lower, the pivots on its diagonal), then L'^T (unit upper)
+    HostCSR F1, F2;
+    std::vector<double2> d1(n);
+    {
+        std::thread tt([&] { F2 = transpose(P.hL, false); });
+        F1 = transpose(P.hU, true);
+        for (int64_t i = 0; i < n; i++) d1[i] = P.hU.val[P.hU.rowptr[i]];
+        tt.join();
+    }
     int64_t levL = 0, levU = 0;
-    std::thread lev([&] { levL = count_levels(P.hL, false); });   // diagnostics, off the path
-    std::thread levu([&] { levU = count_levels(P.hU, true); });
+    std::thread lev([&] { levL = count_levels(F1, false); });   // diagnostics, off the path
+    std::thread levu([&] { levU = count_levels(F2, true); });
     try {
         // the two factors' layouts are independent: build them concurrently (host work of
         // one overlaps the other's copies)
@@ -464,26 +534,19 @@ void setup_problem(Problem& P, double drop_tol, double fill_factor, double permt
         std::thread tl([&] {
             try {
                 SSB_CUDA(cudaSetDevice(P.device));   // the current device is per host thread
-                build_block_tri(P.hL, false, B, QMAX, threads, P.L, s);
+                build_block_tri(F1, d1.data(), false, B, QMAX, threads, P.L, s);
             } catch (...) {
                 errL = std::current_exception();
             }
         });
         try {
-            build_block_tri(P.hU, true, B, QMAX_U, threads, P.U, s);
+            build_block_tri(F2, nullptr, true, B, QMAX_U, threads, P.U, s);
         } catch (...) {
             tl.join();
             throw;
         }
         tl.join();
         if (errL) std::rethrow_exception(errL);
-        bool identity = true;
-        for (int64_t q = 0; q < P.n && identity; q++) identity = P.colperm[q] == q;
-        if (!identity) {   // ILUTP exchanged columns: the U substitution scatters x = Pi y
-            SSB_CUDA(cudaMalloc(&P.U.operm, P.n * sizeof(int64_t)));
-            SSB_CUDA(cudaMalloc(&P.U.xwork, P.n * sizeof(double2)));
-            SSB_CUDA(cudaMemcpy(P.U.operm, P.colperm.data(), P.n * sizeof(int64_t), cudaMemcpyHostToDevice));
-        }
     } catch (...) {
         lev.join();
         levu.join();

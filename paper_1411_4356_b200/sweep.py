@@ -58,6 +58,8 @@ def run_sweep(points: Sequence, rank: int = 0, world: int = 1, group=None,
         return local
     import torch.distributed as dist
 
+    if device is None and dist.get_backend(group) == "nccl":   # NCCL gathers device tensors only
+        device = torch.device("cuda", torch.cuda.current_device())
     t = torch.from_numpy(local)
     if device is not None:
         t = t.to(device)

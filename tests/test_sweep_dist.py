@@ -27,7 +27,8 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, npoints, out_dir):
+def _worker(rank, world, port, npoints, out_dir, explicit_device=False):
+    import torch
     import torch.distributed as dist
 
     from paper_1411_4356_b200.sweep import run_sweep
@@ -37,16 +38,20 @@ def _worker(rank, world, port, npoints, out_dir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         pts = sweep_params(npoints)
-        table = run_sweep(pts, rank, world, solve=fake_solve)
+        # explicit_device: the branch an NCCL group takes (gather from a tensor on a given
+        # device, then back to the host); gloo can only use the CPU device
+        table = run_sweep(pts, rank, world, solve=fake_solve,
+                          device=torch.device("cpu") if explicit_device else None)
         np.save(os.path.join(out_dir, f"r{rank}.npy"), table)
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,npoints", [(2, SWEEP_POINTS), (3, 10), (2, 1)])
-def test_sweep_gather_gloo(tmp_path, world, npoints):
+@pytest.mark.parametrize("world,npoints,explicit_device", [(2, SWEEP_POINTS, False), (3, 10, False), (2, 1, False),
+                                                           (2, SWEEP_POINTS, True)])
+def test_sweep_gather_gloo(tmp_path, world, npoints, explicit_device):
     port = _free_port()
-    mp.spawn(_worker, args=(world, port, npoints, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, port, npoints, str(tmp_path), explicit_device), nprocs=world, join=True)
     pts = sweep_params(npoints)
     ref = np.array([fake_solve(p) for p in pts])
     for r in range(world):
