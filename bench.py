@@ -7,10 +7,16 @@ with the ILUT factors + CGS2 orthogonalisation), the un-permutation/normalisatio
 rho, and the NCCL all-gather of the observables (<a^+a>, <b^+b>) across ranks.
 Setup (build, RCM, ILUT) is done once before the timed region and reported separately.
 
-Default (N = 1): BASELINE configs[1] (N_c=6, N_m=30, Liouvillian dim 32,400).
+Default (N = 1): BASELINE configs[2] (N_c=10, N_m=60, Liouvillian dim 360,000), the
+largest single Liouvillian whose setup fits the bench's time budget (configs[3] is
+measured with --workload large).
 N > 1 (torchrun): every rank solves its own detuning point of the same shape (the
 sweep axis of the north star): weak scaling, no data-path collective except the
-observable gather.  --impl reference times the oracle (oracle/) on host cores.
+observable gather.
+--workload sweep: BASELINE configs[4], the 64-point detuning sweep through
+paper_1411_4356_b200.sweep.run_sweep (contiguous shards over the ranks, observables
+all-gathered over NCCL); a step is the whole sweep, per point build + setup + solve.
+--impl reference times the oracle (oracle/) on host cores.
 """
 from __future__ import annotations
 
@@ -39,8 +45,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="small", choices=["tiny", "small", "medium", "large"])
+    ap.add_argument("--workload", default="medium", choices=["tiny", "small", "medium", "large", "sweep"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-baseline-only", default=None, help=argparse.SUPPRESS)   # internal: the oracle leg
     ap.add_argument("--threads", type=int, default=0, help="host threads for the ILUT setup")
     ap.add_argument("--dims", default="tiny,small,medium",
                     help="configs for the time-to-steady-state vs Liouvillian-dim table (rank 0, N = 1)")
@@ -128,40 +135,45 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(name: str, budget_s: float = 20.0):
-    """The oracle as it stands (numpy/scipy + plain C), timed on host cores: setup untimed,
-    then GMRES Arnoldi steps until ~budget_s; reports oracle GMRES iterations/s."""
+def cpu_baseline(name: str, budget_s: float = 20.0, oracle_state: dict | None = None):
+    """The oracle as it stands (numpy/scipy + plain C), timed on host cores: setup untimed
+    (RCM + the column-oriented iLUTP of R16, cached in oracle_state across calls), then
+    GMRES Arnoldi steps until ~budget_s; reports oracle GMRES iterations/s."""
     from threadpoolctl import threadpool_limits
 
     from oracle import liouvillian as lv
     from oracle import rcm as R
     from oracle import steadystate as ss
-    from oracle.ilut import ilutp
     from oracle.trisolve import apply_preconditioner
     from oracle import gmres as G
 
     p = CONFIGS[name]
-    Lt, rhs, w, L = lv.constrained_system(p)
-    perm = ss.order(Lt)
-    A = R.permute(Lt, perm)
-    F = ilutp(A, p.drop_tol, p.fill_factor, p.permtol)
+    st = oracle_state if oracle_state is not None else {}
+    if "A" not in st:
+        t0 = time.perf_counter()
+        Lt, rhs, w, L = lv.constrained_system(p)
+        perm = ss.order(Lt)
+        A = R.permute(Lt, perm)
+        st.update(A=A, F=ss.factor(A, p), b=rhs[perm], setup_s=time.perf_counter() - t0)
+    A, F, b = st["A"], st["F"], st["b"]
     with threadpool_limits(limits=1):
         # calibrate: time a bounded number of Arnoldi steps (max_iter cap), one cycle at most
         t0 = time.perf_counter()
-        G.gmres(lambda v: A @ v, lambda v: apply_preconditioner(F, v), rhs[perm], p.restart, p.tol, 2)
+        G.gmres(lambda v: A @ v, lambda v: apply_preconditioner(F, v), b, p.restart, p.tol, 2)
         per = (time.perf_counter() - t0) / 2
         k = max(2, min(p.max_iter, int(budget_s / max(per, 1e-6))))
         t0 = time.perf_counter()
-        r = G.gmres(lambda v: A @ v, lambda v: apply_preconditioner(F, v), rhs[perm], p.restart, p.tol, k)
+        r = G.gmres(lambda v: A @ v, lambda v: apply_preconditioner(F, v), b, p.restart, p.tol, k)
         dt = time.perf_counter() - t0
     return {"value": r.iterations / dt, "unit": "iterations/s", "cores": 1, "kind": "oracle",
             "sample": f"{r.iterations} oracle GMRES({p.restart}) Arnoldi steps on {name} "
-                      f"(n={p.liouvillian_dim}) after an untimed oracle setup; {dt:.1f} s, 1 thread"}
+                      f"(n={p.liouvillian_dim}) after an untimed oracle setup ({st['setup_s']:.0f} s); "
+                      f"{dt:.1f} s, 1 thread"}
 
 
 # oracle GMRES iterations to tol from x0 = 0 (tests/test_oracle_gmres.py, oracle.steadystate);
 # the reference arm's ms_per_step is that many steps at its sampled rate
-ORACLE_ITERATIONS = {"tiny": 11, "small": 26}
+ORACLE_ITERATIONS = {"tiny": 11, "small": 26, "medium": 33}   # medium: tests/golden/medium_rho.json
 
 
 def run_reference(args):
@@ -171,8 +183,9 @@ def run_reference(args):
     base = CONFIGS[args.workload]
     vals = []
     cb = None
+    ost = {}
     for step in range(args.warmup + args.steps):
-        cb = cpu_baseline(args.workload, budget_s=max(5.0, 120.0 / (args.warmup + args.steps)))
+        cb = cpu_baseline(args.workload, budget_s=max(5.0, 120.0 / (args.warmup + args.steps)), oracle_state=ost)
         if step >= args.warmup:
             vals.append(cb["value"])
     v = statistics.mean(vals)
@@ -206,6 +219,29 @@ def precond_bytes(si, n):
     pointers, and per factor the right-hand side read, x written and x read back once."""
     strict = si["nnz_L"] + si["nnz_U"] - n
     return strict * 20 + n * 16 + 2 * ((n + 1) * 8 + 3 * n * 16)
+
+
+def spmv_bytes(nnz, n):
+    """One L~x: values + columns, row pointers, x read, y written."""
+    return nnz * 20 + (n + 1) * 8 + 2 * n * 16
+
+
+def cgs_bytes(nv, n):
+    """CGS2 at Arnoldi step j (nv = j + 1 basis vectors): three streaming passes over V,
+    w read three times and written twice (krylov.cu)."""
+    return 3 * nv * n * 16 + 5 * n * 16
+
+
+def solve_bytes(si, build, iterations, restart):
+    """Algorithmic bytes of the Arnoldi steps of one solve (the north star's per-iteration
+    roofline: L~, L, U and the Krylov vectors): every step SpMV + M^{-1} + CGS2 with the
+    basis size of its position in its restart cycle."""
+    n, nnz = build["n"], build["nnz"]
+    per = spmv_bytes(nnz, n) + precond_bytes(si, n)
+    tot = 0
+    for it in range(int(iterations)):
+        tot += per + cgs_bytes(it % restart + 1, n)
+    return tot
 
 
 def steady_state_vs_dim(names, threads):
@@ -249,6 +285,12 @@ def run_b200(args):
     s = pb.SteadyState(p, stream=stream)
     s.setup(threads=args.threads)
     setup_s = time.perf_counter() - t0
+    # the oracle's CPU baseline runs in its own process on the host cores meanwhile (its
+    # untimed iLUTP setup alone takes minutes on the larger configs); one core of work
+    cpu_proc = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu_proc = subprocess.Popen([sys.executable, os.path.abspath(__file__), "--cpu-baseline-only",
+                                     args.workload], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
     n = s.n
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     obs = torch.zeros(2, dtype=torch.float64, device=dev)
@@ -340,6 +382,9 @@ def run_b200(args):
         ms_pc = lvl["trsv_lower"] + lvl["trsv_upper"]
         achieved = bytes_pc / (ms_pc * 1e-3) / 1e9
         tr = ncu_traffic("k_chain_trsv")
+        its_per_solve = it_sum / (args.steps * world)
+        sb = solve_bytes(si, s.build_info, round(its_per_solve), p.restart)
+        ach_it = sb / (ms_max / args.steps * 1e-3) / 1e9
         line = {
             "metric": METRIC, "value": it_sum / (ms_max * 1e-3), "unit": "iterations/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
@@ -357,6 +402,12 @@ def run_b200(args):
                          "kernel_ms": lvl, "trsv_block": si.get("trsv_block"),
                          "trsv_q": [si.get("trsv_q_L"), si.get("trsv_q_U")],
                          "note": "chain-latency bound: n/B dependent block steps per factor (DESIGN.md sec. 5)"},
+            "roofline_iteration": {"bound": "hbm", "what": "whole Arnoldi steps of the solve (SpMV + M^-1 + CGS2): "
+                                   "algorithmic bytes of L~, the factors and the Krylov vectors / solve time",
+                                   "achieved": ach_it, "peak": peak, "unit": "GB/s", "frac": ach_it / peak,
+                                   "bytes_per_solve": sb, "bytes_per_iteration": sb / max(1, round(its_per_solve)),
+                                   "spmv_bytes": spmv_bytes(s.build_info["nnz"], n),
+                                   "precond_bytes": bytes_pc},
             "e2e": {"value": e2e_it_sum / (e2e_max * 1e-3), "unit": "iterations/s",
                     "h2d_bytes_per_step": n * 16, "d2h_bytes_per_step": n * 16},
             "gpu_launches": int(launches),
@@ -364,21 +415,125 @@ def run_b200(args):
         }
         if world == 1 and args.dims:
             line["time_to_steady_state_vs_dim"] = steady_state_vs_dim(args.dims.split(","), args.threads)
-        if not args.no_cpu_baseline and world == 1:
+        if cpu_proc is not None:
             try:
-                line["cpu_baseline"] = cpu_baseline(args.workload)
+                out, _ = cpu_proc.communicate(timeout=1500)
+                line["cpu_baseline"] = json.loads(out.strip().splitlines()[-1])
             except Exception as e:  # the baseline is reported, never required
-                line["cpu_baseline"] = {"value": None, "error": str(e)}
+                cpu_proc.kill()
+                line["cpu_baseline"] = {"value": None, "error": repr(e)}
         print(json.dumps(line), flush=True)
     s.close()
     if world > 1:
         dist.destroy_process_group()
 
 
+def run_sweep_bench(args):
+    """configs[4]: the 64-point detuning sweep through sweep.run_sweep.  A step is the whole
+    sweep: every rank builds, sets up and solves its contiguous shard, one Liouvillian at a
+    time, and the observables of all points are all-gathered over NCCL.  Timed with CUDA
+    events on the rank's stream around the step (host setup included: time to steady
+    state), max over ranks; value = points of the whole job per second."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1411_4356_b200 as pb
+    from paper_1411_4356_b200.sweep import run_sweep, shard_range
+    from workloads import SWEEP_BASE, sweep_params
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        group = dist.group.WORLD
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    points = sweep_params()
+    rec = {"solve_ms": 0.0, "iterations": 0, "setup_s": 0.0, "points": 0}
+
+    def solve(p):
+        t0 = time.perf_counter()
+        s = pb.SteadyState(p, stream=stream).setup(threads=args.threads)
+        rec["setup_s"] += time.perf_counter() - t0
+        s.solve()
+        na, nb = s.expect()
+        i = s.solve_info
+        rec["solve_ms"] += i["solve_ms"]
+        rec["iterations"] += i["iterations"]
+        rec["points"] += 1
+        s.close()
+        return (p.Delta, na, nb, i["iterations"], i["rel_residual"], i["converged"], i["solve_ms"])
+
+    for _ in range(args.warmup):   # warm-up: one point of the rank's shard (context, kernels, allocator)
+        solve(points[shard_range(len(points), rank, world).start])
+    for k in rec:
+        rec[k] = 0 if k != "setup_s" else 0.0
+    rec["solve_ms"] = 0.0
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = pb.ss_kernel_launches()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    tab = None
+    ms = 0.0
+    for _ in range(args.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        tab = run_sweep(points, rank, world, group=group, solve=solve)
+        e1.record(stream)
+        e1.synchronize()
+        ms += e0.elapsed_time(e1)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = pb.ss_kernel_launches() - launches0
+    tt = torch.tensor([ms, rec["solve_ms"], float(rec["iterations"]), rec["setup_s"]], dtype=torch.float64,
+                      device=dev)
+    if world > 1:
+        dist.all_reduce(tt[0:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt[1:4], op=dist.ReduceOp.SUM)
+    ms_max, solve_ms_sum, its_sum, setup_sum = [float(v) for v in tt.tolist()]
+    if rank == 0:
+        npts = len(points) * args.steps
+        conv = int(np.nansum(tab[:, 5]))
+        line = {
+            "metric": METRIC, "value": npts / (ms_max * 1e-3), "unit": "steady states/s (64-point sweep)",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic (BASELINE configs[4] parameter sweep)",
+            "config": {"workload": "configs[4] sweep: 64 detunings in [-2, 2], N_c=8, N_m=60, Liouvillian dim 230400",
+                       "N_c": SWEEP_BASE.N_c, "N_m": SWEEP_BASE.N_m, "drop_tol": SWEEP_BASE.drop_tol,
+                       "fill_factor": SWEEP_BASE.fill_factor, "permtol": SWEEP_BASE.permtol,
+                       "restart": SWEEP_BASE.restart, "tol": SWEEP_BASE.tol, "ranks": world,
+                       "sharding": "contiguous blocks of points per rank; observables all-gathered (NCCL)",
+                       "l2": "inputs (factors of every point) larger than L2"},
+            "converged": conv, "points": len(points),
+            "gmres_iterations_per_s": its_sum / (solve_ms_sum * 1e-3) if solve_ms_sum else None,
+            "solve_s_sum": solve_ms_sum * 1e-3, "setup_s_sum": setup_sum,
+            "table": {"fields": ["Delta", "n_cavity", "n_mech", "iterations", "rel_residual", "converged",
+                                 "solve_ms"], "rows": tab.tolist()},
+            "e2e": {"value": npts / (ms_max * 1e-3), "unit": "steady states/s (64-point sweep)",
+                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": int(len(points) * 7 * 8),
+                    "note": "parameters in, observables out: the step is already end to end"},
+            "gpu_launches": int(launches), "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
+    if args.cpu_baseline_only:
+        print(json.dumps(cpu_baseline(args.cpu_baseline_only)), flush=True)
+        return
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "sweep":
+        run_sweep_bench(args)
     else:
         run_b200(args)
 

@@ -292,11 +292,12 @@ def test_trace_abi(cuda):
 
 def test_full_size_medium(cuda):
     """BASELINE configs[2] (n = 360,000) at full size through the C ABI, in the launch
-    configuration bench.py times: properties that hold at any size (the oracle's direct
-    solve does not fit here) -- the north-star residual of the GPU steady state computed
-    with the oracle's own Liouvillian, Tr rho = 1, rho = rho^H, a real non-negative
-    diagonal -- and the forward substitution checked row by row on sampled rows against
-    its plain definition (y_i + sum_{j<i} l_ij y_j = x_i) with the exported factor."""
+    configuration bench.py times: rho element by element against the oracle's iterative
+    steady state (tests/golden/medium_rho.npy, written by a committed oracle-only script;
+    the oracle's direct solve does not fit here), the north-star residual computed with
+    the oracle's own Liouvillian, Tr rho = 1, rho = rho^H, a real non-negative diagonal,
+    and both substitutions checked row by row on sampled rows against their plain
+    definitions with the exported factors."""
     torch = cuda
     p = CONFIGS["medium"]
     s = pb().SteadyState(p).setup().solve()
@@ -305,6 +306,14 @@ def test_full_size_medium(cuda):
     rho = s.rho().cpu().numpy()
     assert ss.liouvillian_residual(rho, p) <= 1e-9
     assert abs(np.trace(rho) - 1) <= 1e-12
+    # element-wise against the ORACLE's steady state (scripts/make_golden_medium.py: oracle
+    # RCM + column iLUTP + GMRES(50), converged to 3.2e-11; north-star bar 1e-6)
+    import os
+    ref = np.load(os.path.join(os.path.dirname(__file__), "golden", "medium_rho.npy"))
+    assert np.abs(rho - ref).sum() <= 1e-6
+    na, nb = s.expect()
+    ra, rb = ss.expect(ref, p)
+    assert abs(na - ra) <= 1e-8 and abs(nb - rb) <= 1e-8
     # the exact steady state is Hermitian with a real non-negative diagonal, so these
     # deviations are bounded by 2 ||rho - rho_exact||_1, which the north star bounds by
     # 2e-6 (measured: 7e-10)
