@@ -28,16 +28,35 @@ struct DevCSR {
         SSB_CUDA(cudaMalloc(&col, (nnz > 0 ? nnz : 1) * sizeof(int32_t)));
         SSB_CUDA(cudaMalloc(&val, (nnz > 0 ? nnz : 1) * sizeof(double2)));
     }
+    // SELL-32 copy for the SpMV (spmv.cu), built at setup: slice s = rows 32s .. 32s+31,
+    // entries column-major within the slice (entry e of row 32s+r at sptr[s] + 32e + r),
+    // width = the longest row of the slice; padding col 0 / value 0.  Rows longer than
+    // kSellLong entries (the trace row) are left out (first col = -1) and summed from
+    // the CSR by one warp each (lrows).
+    int64_t nslices = 0, nlong = 0, sell_entries = 0;
+    int64_t* sptr = nullptr;
+    int32_t* scol = nullptr;
+    double2* sval = nullptr;
+    int64_t* lrows = nullptr;
     void release() {
         cudaFree(rowptr);
         cudaFree(col);
         cudaFree(val);
+        cudaFree(sptr);
+        cudaFree(scol);
+        cudaFree(sval);
+        cudaFree(lrows);
         rowptr = nullptr;
         col = nullptr;
         val = nullptr;
-        n = nnz = 0;
+        sptr = nullptr;
+        scol = nullptr;
+        sval = nullptr;
+        lrows = nullptr;
+        n = nnz = nslices = nlong = sell_entries = 0;
     }
 };
+constexpr int kSellLong = 64;
 
 // std::vector whose resize() leaves trivial elements uninitialised: the setup fills its
 // large arrays in parallel (first touch) instead of zeroing GBs on one thread first.
@@ -235,6 +254,8 @@ void ilut_factor(const HostCSR& A, double drop_tol, double fill_factor, double p
                  HostCSR& U, std::vector<int64_t>& colperm, IlutStats& st);
 // spmv.cu
 void spmv(const DevCSR& A, const double2* x, double2* y, cudaStream_t s);
+// setup.cpp: the SELL-32 copy of a host CSR into D (D's CSR already uploaded)
+void build_sell(const HostCSR& H, DevCSR& D, cudaStream_t s);
 // trsv.cu: x = T^{-1} b for one factor (b, x in natural index order; x must not alias b)
 // trace (optional, device, SS_TRACE_STAMPS x nblk %globaltimer stamps per block; the
 // meaning of each stamp is listed at ss_debug_trace_trsv in include/ss_b200.h).

@@ -135,6 +135,61 @@ void parallel_for(int64_t n, int threads, Fn fn, int64_t grain = 1024) {
     for (auto& th : pool) th.join();
 }
 
+}  // namespace
+
+void build_sell(const HostCSR& H, DevCSR& D, cudaStream_t s) {
+    const int64_t n = H.n, ns = (n + 31) / 32;
+    std::vector<int64_t> sptr(ns + 1, 0), lrows;
+    for (int64_t sl = 0; sl < ns; sl++) {
+        int64_t w = 1;
+        for (int64_t r = sl * 32; r < std::min(n, sl * 32 + 32); r++) {
+            const int64_t len = H.rowptr[r + 1] - H.rowptr[r];
+            if (len > kSellLong) lrows.push_back(r);
+            else w = std::max(w, len);
+        }
+        sptr[sl + 1] = sptr[sl] + 32 * w;
+    }
+    const int64_t tot = sptr[ns];
+    hvec<int32_t> c(tot);
+    hvec<double2> v(tot);
+    const int threads = (int)std::max(1u, std::thread::hardware_concurrency());
+    parallel_for(ns, threads, [&](int64_t lo, int64_t hi) {
+        for (int64_t sl = lo; sl < hi; sl++) {
+            const int64_t w = (sptr[sl + 1] - sptr[sl]) / 32;
+            for (int r = 0; r < 32; r++) {
+                const int64_t i = sl * 32 + r;
+                const int64_t len = i < n ? H.rowptr[i + 1] - H.rowptr[i] : 0;
+                const bool lng = len > kSellLong;
+                for (int64_t e = 0; e < w; e++) {
+                    const int64_t t = sptr[sl] + 32 * e + r;
+                    if (!lng && e < len) {
+                        c[t] = (int32_t)H.col[H.rowptr[i] + e];
+                        v[t] = H.val[H.rowptr[i] + e];
+                    } else {
+                        c[t] = (lng && e == 0) ? -1 : 0;
+                        v[t] = make_double2(0.0, 0.0);
+                    }
+                }
+            }
+        }
+    }, 256);
+    D.nslices = ns;
+    D.nlong = (int64_t)lrows.size();
+    D.sell_entries = tot;
+    SSB_CUDA(cudaMalloc(&D.sptr, (ns + 1) * sizeof(int64_t)));
+    SSB_CUDA(cudaMalloc(&D.scol, std::max<int64_t>(1, tot) * sizeof(int32_t)));
+    SSB_CUDA(cudaMalloc(&D.sval, std::max<int64_t>(1, tot) * sizeof(double2)));
+    SSB_CUDA(cudaMalloc(&D.lrows, std::max<int64_t>(1, D.nlong) * sizeof(int64_t)));
+    SSB_CUDA(cudaMemcpyAsync(D.sptr, sptr.data(), (ns + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    SSB_CUDA(cudaMemcpyAsync(D.scol, c.data(), tot * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    SSB_CUDA(cudaMemcpyAsync(D.sval, v.data(), tot * sizeof(double2), cudaMemcpyHostToDevice, s));
+    if (D.nlong)
+        SSB_CUDA(cudaMemcpyAsync(D.lrows, lrows.data(), D.nlong * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    SSB_CUDA(cudaStreamSynchronize(s));
+}
+
+namespace {
+
 // Row-level dependency levels of the substitution (diagnostic: the length of the
 // chain a row-level schedule would walk).
 int64_t count_levels(const HostCSR& F, bool upper) {   // F: strict triangle
@@ -500,6 +555,7 @@ void setup_problem(Problem& P, double drop_tol, double fill_factor, double permt
     {
         const HostCSR Ar = permute_rows(A, P.colperm);
         upload(Ar, P.A, s);
+        build_sell(Ar, P.A, s);
     }
     P.rowperm.resize(n);
     P.rhs_pos = -1;

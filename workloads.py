@@ -82,8 +82,10 @@ CONFIGS: dict[str, Params] = {
 CONFIG_ORDER = ["tiny", "small", "medium", "large", "sweep"]
 
 SWEEP_POINTS = 64
+# configs[4] gives no d, p: d = 1e-5 (configs[3]'s), p = 100 (the paper's own detuning
+# sweep, Fig. 4(a-d)); R15 has the study behind the choice.
 SWEEP_BASE = Params(N_c=8, N_m=60, omega_m=1.0, Delta=0.0, kappa=0.5, g0=0.8, E=0.3,
-                    Gamma_m=1e-4, n_th=0.2, w=None, drop_tol=1e-5, fill_factor=40,
+                    Gamma_m=1e-4, n_th=0.2, w=None, drop_tol=1e-5, fill_factor=100,
                     restart=40, tol=1e-10)
 
 
