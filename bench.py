@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-baseline-only", default=None, help=argparse.SUPPRESS)   # internal: the oracle leg
     ap.add_argument("--threads", type=int, default=0, help="host threads for the ILUT setup")
+    ap.add_argument("--concurrent", type=int, default=4,
+                    help="sweep: points solved at the same time per GPU (host threads, SM budgets)")
     ap.add_argument("--dims", default="tiny,small,medium",
                     help="configs for the time-to-steady-state vs Liouvillian-dim table (rank 0, N = 1)")
     return ap.parse_args()
@@ -449,27 +451,27 @@ def run_sweep_bench(args):
         group = dist.group.WORLD
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
+    import threading
+
+    from paper_1411_4356_b200.sweep import concurrent_solver
+
     points = sweep_params()
-    rec = {"solve_ms": 0.0, "iterations": 0, "setup_s": 0.0, "points": 0}
+    rec = {"solve_ms": 0.0, "iterations": 0, "points": 0}
+    lock = threading.Lock()
+    conc = max(1, min(args.concurrent, 8))
+    inner = concurrent_solver(conc)
 
     def solve(p):
-        t0 = time.perf_counter()
-        s = pb.SteadyState(p, stream=stream).setup(threads=args.threads)
-        rec["setup_s"] += time.perf_counter() - t0
-        s.solve()
-        na, nb = s.expect()
-        i = s.solve_info
-        rec["solve_ms"] += i["solve_ms"]
-        rec["iterations"] += i["iterations"]
-        rec["points"] += 1
-        s.close()
-        return (p.Delta, na, nb, i["iterations"], i["rel_residual"], i["converged"], i["solve_ms"])
+        row = inner(p)
+        with lock:
+            rec["solve_ms"] += row[6]
+            rec["iterations"] += row[3]
+            rec["points"] += 1
+        return row
 
     for _ in range(args.warmup):   # warm-up: one point of the rank's shard (context, kernels, allocator)
         solve(points[shard_range(len(points), rank, world).start])
-    for k in rec:
-        rec[k] = 0 if k != "setup_s" else 0.0
-    rec["solve_ms"] = 0.0
+    rec.update(solve_ms=0.0, iterations=0, points=0)
     clocks = ClockSampler(local)
     clocks.start()
     launches0 = pb.ss_kernel_launches()
@@ -481,7 +483,7 @@ def run_sweep_bench(args):
     for _ in range(args.steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        tab = run_sweep(points, rank, world, group=group, solve=solve)
+        tab = run_sweep(points, rank, world, group=group, solve=solve, concurrent=conc)
         e1.record(stream)
         e1.synchronize()
         ms += e0.elapsed_time(e1)
@@ -490,12 +492,11 @@ def run_sweep_bench(args):
         dist.barrier()
     clk = clocks.stop()
     launches = pb.ss_kernel_launches() - launches0
-    tt = torch.tensor([ms, rec["solve_ms"], float(rec["iterations"]), rec["setup_s"]], dtype=torch.float64,
-                      device=dev)
+    tt = torch.tensor([ms, rec["solve_ms"], float(rec["iterations"])], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tt[0:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(tt[1:4], op=dist.ReduceOp.SUM)
-    ms_max, solve_ms_sum, its_sum, setup_sum = [float(v) for v in tt.tolist()]
+        dist.all_reduce(tt[1:3], op=dist.ReduceOp.SUM)
+    ms_max, solve_ms_sum, its_sum = [float(v) for v in tt.tolist()]
     if rank == 0:
         npts = len(points) * args.steps
         conv = int(np.nansum(tab[:, 5]))
@@ -509,10 +510,12 @@ def run_sweep_bench(args):
                        "fill_factor": SWEEP_BASE.fill_factor, "permtol": SWEEP_BASE.permtol,
                        "restart": SWEEP_BASE.restart, "tol": SWEEP_BASE.tol, "ranks": world,
                        "sharding": "contiguous blocks of points per rank; observables all-gathered (NCCL)",
+                       "concurrent_per_gpu": conc,
                        "l2": "inputs (factors of every point) larger than L2"},
             "converged": conv, "points": len(points),
-            "gmres_iterations_per_s": its_sum / (solve_ms_sum * 1e-3) if solve_ms_sum else None,
-            "solve_s_sum": solve_ms_sum * 1e-3, "setup_s_sum": setup_sum,
+            "concurrent_per_gpu": conc,
+            "gmres_iterations_per_s_per_point": its_sum / (solve_ms_sum * 1e-3) if solve_ms_sum else None,
+            "solve_s_sum": solve_ms_sum * 1e-3,
             "table": {"fields": ["Delta", "n_cavity", "n_mech", "iterations", "rel_residual", "converged",
                                  "solve_ms"], "rows": tab.tolist()},
             "e2e": {"value": npts / (ms_max * 1e-3), "unit": "steady states/s (64-point sweep)",

@@ -106,10 +106,12 @@ typedef struct ss_solve_info {
 int ss_build(const ss_params* p, void* cuda_stream, ss_problem** out, ss_build_info* info);
 
 /* One-time setup: RCM ordering of pattern(L~ + L~^T) (sec. III), the
- * symmetric permutation L~_RCM, the iLUTP(drop_tol, fill_factor, permtol) factors
- * L~_RCM Pi ~ L U (sec. II, "dual-threshold and pivoting"; rules R4-R7, R13
- * of DESIGN.md; permtol = 0: no column exchanges = plain ILUT), the block layout of the
- * substitutions and its upload.  n_threads <= 0 -> all host cores (more than the host
+ * symmetric permutation L~_RCM, the column-oriented iLUTP(drop_tol, fill_factor, permtol)
+ * of L~_RCM (sec. II, "dual-threshold and pivoting", SuperLU's orientation,
+ * PAPER.md:119; R4-R7, R13, R16): the row-wise iLUTP of its transpose,
+ * L~_RCM^T Pi ~ L' U', so Pi^T L~_RCM ~ U'^T L'^T (permtol = 0: no exchanges = plain
+ * ILUT); the operator of the hot path A' = Pi^T L~_RCM (rows in pivot order, SELL-32
+ * copy for the SpMV), the block layout of the two substitutions and their upload.  n_threads <= 0 -> all host cores (more than the host
  * cores are clamped to that; the factors are the same for any n_threads).  May be called again
  * with other parameters.  Errors: SS_ERR_ARG (negative parameter), SS_ERR_BREAKDOWN
  * (zero pivot with drop_tol = 0). */
@@ -143,21 +145,23 @@ const char* ss_last_error(void);
 /* Dimensions: n, nnz(L~); after ss_setup also nnz_L, nnz_U (else -1). */
 int ss_sizes(const ss_problem* h, int64_t* n, int64_t* nnz, int64_t* nnz_L, int64_t* nnz_U);
 
-/* Copy L~ (which = 0: natural order; 1: RCM order, needs ss_setup) to host CSR arrays:
- * rowptr[n+1], colidx[nnz] (int64), vals[2*nnz] (complex128). Columns ascending. */
+/* Copy L~ (which = 0: natural order; 1: the hot path's operator A' = Pi^T L~_RCM, i.e.
+ * row j = row colperm[j] of L~_RCM, needs ss_setup) to host CSR arrays: rowptr[n+1],
+ * colidx[nnz] (int64), vals[2*nnz] (complex128).  Columns ascending. */
 int ss_export_matrix(const ss_problem* h, int32_t which, int64_t* rowptr, int64_t* colidx,
                      double* vals);
 
 /* Copy the RCM permutation perm[n] (new -> old: L~_RCM = L~[perm][:, perm]). */
 int ss_export_perm(const ss_problem* h, int64_t* perm);
 
-/* Copy the iLUTP column permutation colperm[n] (position -> column of L~_RCM:
- * L~_RCM[:, colperm] ~ L U; the identity when no column was exchanged). */
+/* Copy the iLUTP pivot permutation colperm[n]: L~_RCM^T[:, colperm] ~ L' U' (R16), i.e.
+ * row j of A' is row colperm[j] of L~_RCM; the identity when nothing was exchanged. */
 int ss_export_colperm(const ss_problem* h, int64_t* colperm);
 
-/* Copy an ILU factor to host CSR: which = 0: strict lower L (unit diagonal implicit),
- * rowptr[n+1], colidx[nnz_L], vals[2 nnz_L]; which = 1: U with its diagonal FIRST in
- * every row then strict upper columns ascending, rowptr[n+1], colidx[nnz_U], vals[2 nnz_U]. */
+/* Copy an iLUTP factor of L~_RCM^T to host CSR: which = 0: strict lower L' (unit
+ * diagonal implicit), rowptr[n+1], colidx[nnz_L], vals[2 nnz_L]; which = 1: U' with its
+ * diagonal FIRST in every row then strict upper columns ascending, rowptr[n+1],
+ * colidx[nnz_U], vals[2 nnz_U].  M'^{-1} = L'^{-T} U'^{-T}. */
 int ss_export_factors(const ss_problem* h, int32_t which, int64_t* rowptr, int64_t* colidx,
                       double* vals);
 
@@ -176,10 +180,11 @@ int ss_ilutp_host(int64_t n, const int64_t* rowptr, const int64_t* colidx, const
                   double* L_vals, int64_t L_cap, int64_t* U_rowptr, int64_t* U_colidx, double* U_vals,
                   int64_t U_cap, int64_t* colperm);
 
-/* y = L~_RCM x  (device pointers, complex128 length n).                           */
+/* y = A' x = Pi^T L~_RCM x  (device pointers, complex128 length n).                */
 int ss_spmv(ss_problem* h, const void* x_dev, void* y_dev);
-/* y = L^{-1} x (which = 0), y = Pi U^{-1} x (which = 1), y = M^{-1} x = Pi U^{-1} L^{-1} x
- * (which = 2), Pi the iLUTP column permutation (ss_export_colperm);
+/* y = U'^{-T} x (which = 0, the first substitution: lower, the pivots on its diagonal),
+ * y = L'^{-T} x (which = 1, unit upper), y = M'^{-1} x = L'^{-T} U'^{-T} x (which = 2);
+ * M'^{-1} A' = M^{-1} L~_RCM with M = Pi U'^T L'^T (R16);
  * device pointers, length n, x and y may not alias.  which | SS_PRECOND_ASYNC: return
  * right after the launches (stream-ordered, no host synchronisation; used to time the
  * kernels with events).  which = 2 uses the handle's Krylov scratch vector.          */
@@ -199,6 +204,15 @@ int ss_precond(ss_problem* h, int32_t which, const void* x_dev, void* y_dev);
 #define SS_TRACE_STAMPS 16
 int ss_debug_trace_trsv(ss_problem* h, int32_t which, const void* x_dev, void* y_dev, uint64_t* host_trace,
                         int64_t* nblk_out);
+
+/* Limit the substitution kernels of this problem to `sms` SMs (rounded down to whole
+ * 8-CTA clusters, at least 2 clusters; 0 = the whole GPU, the default), so that several
+ * problems can run their solves concurrently on one GPU from different host threads and
+ * streams (the detuning sweep: "several simulations to be
+ * run in parallel").  The launches of one problem spin on each other's CTAs, so the
+ * budgets of the problems solved at the same time must add up to at most the GPU's
+ * co-resident clusters.  Takes effect at the next substitution.  Errors: SS_ERR_ARG. */
+int ss_set_sm_budget(ss_problem* h, int32_t sms);
 
 /* Number of CUDA kernels this library has launched since load (gpu_launches evidence). */
 int64_t ss_kernel_launches(void);

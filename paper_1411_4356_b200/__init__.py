@@ -13,12 +13,12 @@ from __future__ import annotations
 from . import _lib
 from ._lib import (SSError, ss_build, ss_setup, ss_solve, ss_expect, ss_get_rho, ss_solve_host,
                    ss_destroy, ss_sizes, ss_export_matrix, ss_export_perm, ss_export_colperm, ss_export_factors, ss_spmv,
-                   ss_precond, ss_kernel_launches, ss_debug_trace_trsv, ss_ilutp_host)
+                   ss_precond, ss_kernel_launches, ss_debug_trace_trsv, ss_ilutp_host, ss_set_sm_budget)
 
 __all__ = ["SteadyState", "SSError", "ss_build", "ss_setup", "ss_solve", "ss_expect", "ss_get_rho",
            "ss_solve_host", "ss_destroy", "ss_sizes", "ss_export_matrix", "ss_export_perm", "ss_export_colperm",
            "ss_export_factors", "ss_spmv", "ss_precond", "ss_kernel_launches", "ss_debug_trace_trsv",
-           "ss_ilutp_host"]
+           "ss_ilutp_host", "ss_set_sm_budget"]
 
 
 class SteadyState:
@@ -29,7 +29,7 @@ class SteadyState:
     ``expect()`` the observables (<a^+a>, <b^+b>).
     """
 
-    def __init__(self, params, stream=None):
+    def __init__(self, params, stream=None, sm_budget: int = 0):
         import torch
         if not torch.cuda.is_available():
             raise SSError(2, "no CUDA device: the B200 path has no CPU fallback")
@@ -38,6 +38,8 @@ class SteadyState:
         self.torch = torch
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         self.handle, self.build_info = ss_build(params, self.stream.cuda_stream)
+        if sm_budget:
+            ss_set_sm_budget(self.handle, sm_budget)
         self.setup_info = None
         self.solve_info = None
 

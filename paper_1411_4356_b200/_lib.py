@@ -81,6 +81,7 @@ SIGNATURES = [
     ("ss_spmv", ctypes.c_int, [P, P, P]),
     ("ss_precond", ctypes.c_int, [P, I32, P, P]),
     ("ss_kernel_launches", ctypes.c_int64, []),
+    ("ss_set_sm_budget", ctypes.c_int, [P, I32]),
     ("ss_debug_trace_trsv", ctypes.c_int, [P, I32, P, P, P, PI64]),
     ("ss_ilutp_host", ctypes.c_int, [ctypes.c_int64, P, P, P, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                      I32, P, P, P, ctypes.c_int64, P, P, P, ctypes.c_int64, P]),
@@ -137,6 +138,10 @@ def ss_export_colperm(h) -> np.ndarray:
     perm = np.empty(n, np.int64)
     _check(load().ss_export_colperm(h, perm.ctypes.data))
     return perm
+
+
+def ss_set_sm_budget(h, sms: int) -> None:
+    _check(load().ss_set_sm_budget(h, int(sms)))
 
 
 def ss_solve(h, restart: int, tol: float, max_iter: int) -> dict:

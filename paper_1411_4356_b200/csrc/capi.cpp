@@ -159,6 +159,14 @@ int ss_solve_host(ss_problem* h, const double* rhs_host, double* x_host, int32_t
     SS_GUARD_END
 }
 
+int ss_set_sm_budget(ss_problem* h, int32_t sms) {
+    SS_GUARD_BEGIN
+    SSB_CHECK(h && sms >= 0, SS_ERR_ARG, "ss_set_sm_budget: NULL handle or negative budget");
+    h->P.sm_budget = sms;
+    h->P.L.sm_budget = h->P.U.sm_budget = sms;
+    SS_GUARD_END
+}
+
 int ss_expect(ss_problem* h, double* n_cavity, double* n_mech) {
     SS_GUARD_BEGIN
     SSB_CHECK(h && n_cavity && n_mech, SS_ERR_ARG, "ss_expect: NULL argument");

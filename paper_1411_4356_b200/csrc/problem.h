@@ -151,7 +151,8 @@ struct DevBlockTri {
     int64_t* operm = nullptr;   // U of ILUTP: out[operm[p]] = x[p] (column permutation), else null
     double2* xwork = nullptr;   // position-space x when operm is set
     uint32_t epoch = 0;
-    int grid = 0;
+    int grid = 0;         // persistent grid on the whole GPU (all co-resident clusters, <= blocks)
+    int sm_budget = 0;    // ss_set_sm_budget: at most this many CTAs (whole clusters), 0 = grid
     int64_t nlev = 0;   // row-level dependency levels (diagnostic)
     TriArgs args() const {
         return TriArgs{n,         nblk,      rev,  B, farptr, fcol,  fval,  nearB.bp, nearB.col, nearB.val,
@@ -224,6 +225,7 @@ struct Problem {
 
     HostCSR hL, hU;             // iLUTP of L~_RCM^T (export / tests): L~_RCM^T[:, colperm] ~ hL hU
     std::vector<int64_t> colperm;   // its column permutation = the row order of A'
+    int sm_budget = 0;          // ss_set_sm_budget (copied into L, U)
     DevBlockTri L, U;           // the substitutions: L <- U'^T (lower, pivots), U <- L'^T (unit upper)
     int64_t bw_nat = 0, bw_rcm = 0;
 

@@ -610,6 +610,7 @@ void setup_problem(Problem& P, double drop_tol, double fill_factor, double permt
     }
     lev.join();
     levu.join();
+    P.L.sm_budget = P.U.sm_budget = P.sm_budget;
     P.L.nlev = levL;
     P.U.nlev = levU;
     const double t3 = now_ms();

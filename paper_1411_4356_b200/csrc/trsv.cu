@@ -899,7 +899,7 @@ void prepare(DevBlockTri& T) {
     int dev = 0, sms = 0;
     SSB_CUDA(cudaGetDevice(&dev));
     SSB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    // clusters of 4 (chain + 3 lieutenants, then helpers), one CTA per SM; every cluster
+    // clusters of 8 (chain + 7 lieutenants, then helpers), one CTA per SM; every cluster
     // must be resident at once (the CTAs spin on one another)
     cudaLaunchAttribute attr[1];
     cudaLaunchConfig_t cfg = launch_config<B>((sms / C::kCluster) * C::kCluster, attr);
@@ -913,14 +913,18 @@ void prepare(DevBlockTri& T) {
 
 template <int B>
 void launch(DevBlockTri& T, const double2* b, double2* x, cudaStream_t s, unsigned long long* trace) {
+    using C = Cfg<B>;
     auto fn = k_chain_trsv<B>;
     if (T.grid == 0) prepare<B>(T);
     T.epoch++;
     TriArgs a = T.args();
     uint32_t ep = T.epoch;
     double2* xw = T.operm ? T.xwork : x;
+    int grid = T.grid;
+    if (T.sm_budget > 0)   // several problems share the GPU: whole clusters, chain + >= 1 helper cluster
+        grid = std::min(grid, std::max(2 * C::kCluster, (T.sm_budget / C::kCluster) * C::kCluster));
     cudaLaunchAttribute attr[1];
-    cudaLaunchConfig_t cfg = launch_config<B>(T.grid, attr);
+    cudaLaunchConfig_t cfg = launch_config<B>(grid, attr);
     cfg.stream = s;
     SSB_CUDA(cudaLaunchKernelEx(&cfg, fn, a, b, x, xw, ep, trace));
     SSB_LAUNCHED();

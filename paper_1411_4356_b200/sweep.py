@@ -29,12 +29,21 @@ def shard_range(npoints: int, rank: int, world: int) -> range:
     return range(lo, hi)
 
 
-def solve_point_gpu(p) -> tuple:
-    """Build -> setup -> solve -> expect one parameter point on the current CUDA device."""
-    from . import SteadyState
+def solve_point_gpu(p, concurrent: int = 1, host_threads: int = 0, stream=None) -> tuple:
+    """Build -> setup -> solve -> expect one parameter point on the current CUDA device.
 
-    s = SteadyState(p).setup().solve()
+    concurrent > 1: this point shares the GPU with concurrent - 1 others solved from other
+    host threads at the same time -- its substitution kernels get 1/concurrent of the
+    co-resident clusters (ss_set_sm_budget; the budgets add up to at most the GPU, so the
+    persistent launches of different points never wait on one another) and its own stream."""
+    from . import SteadyState, ss_set_sm_budget
+
+    s = SteadyState(p, stream=stream).setup(threads=host_threads)
     try:
+        if concurrent > 1:
+            clusters = s.setup_info["trsv_grid"] // 8          # co-resident clusters (whole GPU)
+            ss_set_sm_budget(s.handle, 8 * max(2, clusters // concurrent))
+        s.solve()
         na, nb = s.expect()
         i = s.solve_info
         return (p.Delta, na, nb, i["iterations"], i["rel_residual"], i["converged"], i["solve_ms"])
@@ -42,18 +51,50 @@ def solve_point_gpu(p) -> tuple:
         s.close()
 
 
+def concurrent_solver(concurrent: int, host_cores: int | None = None) -> Callable:
+    """A solve(p) for run_sweep that may be called from `concurrent` host threads at once:
+    each call on the calling thread's own CUDA stream (same device as the caller of
+    run_sweep), with 1/concurrent of the GPU's co-resident clusters for its substitutions
+    and 1/concurrent of the host cores for its iLUTP setup."""
+    import os
+    import threading
+
+    import torch
+
+    dev = torch.cuda.current_device()
+    cores = host_cores or os.cpu_count() or 1
+    local = threading.local()
+
+    def solve(p):
+        torch.cuda.set_device(dev)
+        if not hasattr(local, "stream"):
+            local.stream = torch.cuda.Stream(device=dev)
+        return solve_point_gpu(p, concurrent, max(1, cores // concurrent), local.stream)
+
+    return solve
+
+
 def run_sweep(points: Sequence, rank: int = 0, world: int = 1, group=None,
-              solve: Callable = solve_point_gpu, device=None) -> np.ndarray:
+              solve: Callable = solve_point_gpu, device=None, concurrent: int = 1) -> np.ndarray:
     """Solve this rank's shard of ``points`` and return the full (npoints x len(FIELDS))
     table on every rank.  ``group`` is a torch.distributed process group (None with
     world == 1).  ``solve(p)`` returns one FIELDS tuple; it is injectable so the host
-    logic runs in tests without a GPU."""
+    logic runs in tests without a GPU.  concurrent > 1: the shard's points are handed
+    out in order to that many host threads calling ``solve`` at once (with the GPU
+    solver: ``concurrent_solver(concurrent)``)."""
     import torch
 
     n = len(points)
     local = np.full((n, len(FIELDS)), np.nan)
-    for k in shard_range(n, rank, world):
-        local[k] = solve(points[k])
+    mine = list(shard_range(n, rank, world))
+    if concurrent > 1 and len(mine) > 1:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=concurrent) as ex:
+            for k, row in zip(mine, ex.map(lambda k: solve(points[k]), mine)):
+                local[k] = row
+    else:
+        for k in mine:
+            local[k] = solve(points[k])
     if world == 1:
         return local
     import torch.distributed as dist

@@ -276,6 +276,33 @@ def test_sweep_points_on_gpu(cuda):
         assert abs(row[1] - ra) <= 1e-7 and abs(row[2] - rb) <= 1e-6
 
 
+def test_concurrent_points_identical_to_sequential(cuda):
+    """Several points solved at the same time on one GPU (sweep.concurrent_solver: host
+    threads, own streams, SM budgets for the persistent substitutions) give exactly the
+    table of the one-at-a-time sweep: the block substitution's reductions have a fixed
+    order whatever the number of helper CTAs, so the results are bit-identical."""
+    from paper_1411_4356_b200.sweep import run_sweep, concurrent_solver
+    pts = [CONFIGS["small"].with_(Delta=d) for d in (-1.0, -0.5, 0.0, 0.5, 1.0)]
+    seq = run_sweep(pts)
+    con = run_sweep(pts, solve=concurrent_solver(3), concurrent=3)
+    assert np.array_equal(seq[:, :6], con[:, :6])      # all but the timing column
+    assert np.all(con[:, 5] == 1.0)
+
+
+def test_sm_budget_same_result(cuda):
+    """ss_set_sm_budget (2 clusters: chain + one helper cluster) leaves M^{-1} bit-identical."""
+    torch = cuda
+    s = pb().SteadyState(CONFIGS["small"]).setup()
+    x = torch.from_numpy(rand_cvec(s.n, 3)).cuda()
+    y0 = s.precond(x, 2)
+    pb().ss_set_sm_budget(s.handle, 16)
+    y1 = s.precond(x, 2)
+    assert torch.equal(y0, y1)
+    with pytest.raises(pb().SSError):
+        pb().ss_set_sm_budget(s.handle, -1)
+    s.close()
+
+
 def test_trace_abi(cuda):
     """ss_debug_trace_trsv returns one row of SS_TRACE_STAMPS (16) stamps per block."""
     torch = cuda

@@ -27,7 +27,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, npoints, out_dir, explicit_device=False):
+def _worker(rank, world, port, npoints, out_dir, explicit_device=False, concurrent=1):
     import torch
     import torch.distributed as dist
 
@@ -41,17 +41,19 @@ def _worker(rank, world, port, npoints, out_dir, explicit_device=False):
         # explicit_device: the branch an NCCL group takes (gather from a tensor on a given
         # device, then back to the host); gloo can only use the CPU device
         table = run_sweep(pts, rank, world, solve=fake_solve,
-                          device=torch.device("cpu") if explicit_device else None)
+                          device=torch.device("cpu") if explicit_device else None, concurrent=concurrent)
         np.save(os.path.join(out_dir, f"r{rank}.npy"), table)
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,npoints,explicit_device", [(2, SWEEP_POINTS, False), (3, 10, False), (2, 1, False),
-                                                           (2, SWEEP_POINTS, True)])
-def test_sweep_gather_gloo(tmp_path, world, npoints, explicit_device):
+@pytest.mark.parametrize("world,npoints,explicit_device,concurrent",
+                         [(2, SWEEP_POINTS, False, 1), (3, 10, False, 1), (2, 1, False, 1),
+                          (2, SWEEP_POINTS, True, 1), (3, SWEEP_POINTS, False, 4)])
+def test_sweep_gather_gloo(tmp_path, world, npoints, explicit_device, concurrent):
     port = _free_port()
-    mp.spawn(_worker, args=(world, port, npoints, str(tmp_path), explicit_device), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, port, npoints, str(tmp_path), explicit_device, concurrent), nprocs=world,
+             join=True)
     pts = sweep_params(npoints)
     ref = np.array([fake_solve(p) for p in pts])
     for r in range(world):
@@ -75,3 +77,24 @@ def test_sweep_points_match_baseline():
     d = np.diff([p.Delta for p in pts])
     assert np.allclose(d, 4.0 / 63)
     assert all(p.N_c == 8 and p.N_m == 60 and p.liouvillian_dim == 230400 for p in pts)
+
+
+def test_concurrent_threads_fill_the_same_table():
+    """concurrent > 1 hands the rank's points to host threads: every point solved once,
+    each row where the sequential sweep puts it."""
+    import threading
+
+    from paper_1411_4356_b200.sweep import run_sweep
+    pts = sweep_params(13)
+    seen = []
+    lock = threading.Lock()
+
+    def solve(p):
+        with lock:
+            seen.append(p.Delta)
+        return fake_solve(p)
+
+    seq = run_sweep(pts, solve=fake_solve)
+    con = run_sweep(pts, solve=solve, concurrent=4)
+    assert np.array_equal(seq, con)
+    assert sorted(seen) == sorted(p.Delta for p in pts)
