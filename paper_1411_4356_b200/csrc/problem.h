@@ -124,6 +124,9 @@ struct TriArgs {
     const int64_t* farptr;    // [n+1] entries of row i' with source block <= k-Q_k (k = i'/B)
     const int32_t* fcol;      //       kernel-space columns, ascending within a row
     const double2* fval;
+    const int64_t* itemptr;   // [nblk+1] far work items of block k: items[itemptr[k] .. itemptr[k+1])
+    const uint32_t* items;    //          item = (c << 5) | r: entries 32c .. 32c+31 of row r of the
+                              //          block's far part, sorted by newest source block (setup.cpp)
     const int64_t* nbpB;      // near list B: [nblk*kLieutenants+1], list of (block k, lieutenant l) at k*kLt+l
     const int32_t* ncolB;
     const double2* nvalB;
@@ -142,6 +145,8 @@ struct DevBlockTri {
     int64_t* farptr = nullptr;
     int32_t* fcol = nullptr;
     double2* fval = nullptr;
+    int64_t* itemptr = nullptr;
+    uint32_t* items = nullptr;
     NearDev nearB;
     double2* dinv = nullptr;
     double2* G = nullptr;
@@ -155,13 +160,15 @@ struct DevBlockTri {
     int sm_budget = 0;    // ss_set_sm_budget: at most this many CTAs (whole clusters), 0 = grid
     int64_t nlev = 0;   // row-level dependency levels (diagnostic)
     TriArgs args() const {
-        return TriArgs{n,         nblk,      rev,  B, farptr, fcol,  fval,  nearB.bp, nearB.col, nearB.val,
-                       nearB.loc, dinv,      G,    yfar,  operm,  fflag, xfront};
+        return TriArgs{n,        nblk,      rev,       B,         farptr, fcol, fval,  itemptr, items, nearB.bp,
+                       nearB.col, nearB.val, nearB.loc, dinv,      G,      yfar, operm, fflag,   xfront};
     }
     void release() {
         cudaFree(farptr);
         cudaFree(fcol);
         cudaFree(fval);
+        cudaFree(itemptr);
+        cudaFree(items);
         nearB.release();
         cudaFree(dinv);
         cudaFree(G);

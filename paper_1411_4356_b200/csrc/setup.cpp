@@ -352,6 +352,38 @@ void build_block_tri(const HostCSR& F, const double2* diag, bool upper, int B, i
     for (int64_t i = 0; i < n; i++) T.nnz_near += nin[i] - cnt[i];
     T.nnz_strict = F.nnz();
 
+    // far work items of each block for the helper CTAs: item (r, c) = far entries 32c ..
+    // 32c+31 of the block's row r, keyed by the source block of its last (newest) entry and
+    // sorted by that key (then c, r), so that a block's long rows are spread over all helper
+    // warps and the items waiting for the newest x blocks come last
+    static_assert(sizeof(uint32_t) == 4, "item encoding (c << 5) | r needs B = 32");
+    SSB_CHECK(B == 32, SS_ERR_ARG, "far work items encode the row in 5 bits (B = 32)");
+    std::vector<int64_t> itemptr(nblk + 1, 0);
+    for (int64_t k = 0; k < nblk; k++) {
+        int64_t c = 0;
+        for (int64_t ip = k * B; ip < std::min(n, (k + 1) * B); ip++) c += (cnt[ip] + 31) / 32;
+        itemptr[k + 1] = itemptr[k] + c;
+    }
+    hvec<uint32_t> items(std::max<int64_t>(1, itemptr[nblk]));
+    parallel_for(nblk, threads, [&](int64_t lo, int64_t hi) {
+        std::vector<std::pair<int64_t, uint32_t>> key;
+        for (int64_t k = lo; k < hi; k++) {
+            key.clear();
+            for (int64_t ip = k * B; ip < std::min(n, (k + 1) * B); ip++) {
+                int64_t q0, q1;
+                row_range(ip, q0, q1);
+                const uint32_t r = (uint32_t)(ip - k * B);
+                for (int64_t c = 0; c * 32 < cnt[ip]; c++) {
+                    const int64_t last = std::min(cnt[ip], 32 * c + 32) - 1;   // far entries lead the row
+                    const int64_t src = kcol(entry(q0, q1, last)) / B;
+                    key.emplace_back((src << 32) | (c << 5) | r, (uint32_t)((c << 5) | r));
+                }
+            }
+            std::sort(key.begin(), key.end());
+            for (size_t t = 0; t < key.size(); t++) items[itemptr[k] + t] = key[t].second;
+        }
+    }, 64);
+
     auto upload_near = [&](const NearHost& H, int64_t total, NearDev& D) {
         SSB_CUDA(cudaMalloc(&D.bp, H.bp.size() * sizeof(int64_t)));
         SSB_CUDA(cudaMalloc(&D.col, std::max<int64_t>(4, total) * sizeof(int32_t)));
@@ -374,6 +406,10 @@ void build_block_tri(const HostCSR& F, const double2* diag, bool upper, int B, i
     SSB_CUDA(cudaMemsetAsync(T.fflag, 0, std::max<int64_t>(1, nblk) * sizeof(uint32_t), s));
     SSB_CUDA(cudaMemsetAsync(T.xfront, 0, sizeof(unsigned long long), s));
     SSB_CUDA(cudaMemcpyAsync(T.farptr, farptr.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    SSB_CUDA(cudaMalloc(&T.itemptr, (nblk + 1) * sizeof(int64_t)));
+    SSB_CUDA(cudaMalloc(&T.items, items.size() * sizeof(uint32_t)));
+    SSB_CUDA(cudaMemcpyAsync(T.itemptr, itemptr.data(), (nblk + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    SSB_CUDA(cudaMemcpyAsync(T.items, items.data(), items.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
     SSB_CUDA(cudaStreamSynchronize(s));
 
     // entries, in block chunks of ~2^26 (bounded host staging); the rows of a chunk of
@@ -419,13 +455,17 @@ void build_block_tri(const HostCSR& F, const double2* diag, bool upper, int B, i
         });
         const double tc0 = now_ms();
         if (flen) {
-            SSB_CUDA(cudaMemcpy(T.fcol + fb, fc.data(), flen * sizeof(int32_t), cudaMemcpyHostToDevice));
-            SSB_CUDA(cudaMemcpy(T.fval + fb, fv.data(), flen * sizeof(double2), cudaMemcpyHostToDevice));
+            SSB_CUDA(cudaMemcpyAsync(T.fcol + fb, fc.data(), flen * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+            SSB_CUDA(cudaMemcpyAsync(T.fval + fb, fv.data(), flen * sizeof(double2), cudaMemcpyHostToDevice, s));
         }
         if (blen > 0) {
-            SSB_CUDA(cudaMemcpy(T.nearB.col + bb, bc.data(), blen * sizeof(int32_t), cudaMemcpyHostToDevice));
-            SSB_CUDA(cudaMemcpy(T.nearB.val + bb, bv.data(), blen * sizeof(double2), cudaMemcpyHostToDevice));
+            SSB_CUDA(cudaMemcpyAsync(T.nearB.col + bb, bc.data(), blen * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+            SSB_CUDA(cudaMemcpyAsync(T.nearB.val + bb, bv.data(), blen * sizeof(double2), cudaMemcpyHostToDevice, s));
         }
+        // on the problem's stream, complete before the staging buffers are refilled: a plain
+        // cudaMemcpy from pageable memory runs on the legacy stream and may still be in flight
+        // when it returns, unordered with a non-blocking stream (concurrent sweep points)
+        SSB_CUDA(cudaStreamSynchronize(s));
         t_copy += now_ms() - tc0;
         k0 = k1;
     }
@@ -512,9 +552,11 @@ void build_block_tri(const HostCSR& F, const double2* diag, bool upper, int B, i
                 }
             }
         }, 4);
-        SSB_CUDA(cudaMemcpy(T.dinv + k0 * PK, ibuf.data(), (k1 - k0) * PK * sizeof(double2), cudaMemcpyHostToDevice));
-        SSB_CUDA(cudaMemcpy(T.G + k0 * kDense * B * B, gbuf.data(), (k1 - k0) * kDense * B * B * sizeof(double2),
-                            cudaMemcpyHostToDevice));
+        SSB_CUDA(cudaMemcpyAsync(T.dinv + k0 * PK, ibuf.data(), (k1 - k0) * PK * sizeof(double2),
+                                 cudaMemcpyHostToDevice, s));
+        SSB_CUDA(cudaMemcpyAsync(T.G + k0 * kDense * B * B, gbuf.data(), (k1 - k0) * kDense * B * B * sizeof(double2),
+                                 cudaMemcpyHostToDevice, s));
+        SSB_CUDA(cudaStreamSynchronize(s));   // (as above: the problem's stream, buffers reused)
     }
     SSB_CUDA(cudaStreamSynchronize(s));
     block_trsv_prepare(T);

@@ -775,12 +775,24 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
     }
 
     // ================================================================ helper CTAs
+    // The far part of block k is cut into work items (row r, 32-entry chunk c), sorted at
+    // setup by the newest source block they read (setup.cpp); warp w takes items w, w+16,
+    // ..., kHU at a time (their column/value loads in flight together), waits once for the
+    // newest source block of the batch, gathers x, and adds each item's warp sum to its
+    // per-warp row partial (lane 0, item order: deterministic).  A block's long rows are so
+    // spread over all 16 warps, and the items gated by the newest x blocks come last.
     if (warp >= C::kFarWarps) return;
+    constexpr int kHU = 4;
     const int H = gridDim.x - C::kCluster;
     int64_t* sRowP = reinterpret_cast<int64_t*>(smem + C::kOffRowP);
     int32_t* sRowL = reinterpret_cast<int32_t*>(smem + C::kOffRowL);
     double2* sRf = reinterpret_cast<double2*>(smem + C::kOffR);   // b_k - far part
     const double2* hInv = reinterpret_cast<const double2*>(smem);  // D_k^{-1}, staged by TMA
+    // per-warp row partials of the far sums, in the stage region after D_k^{-1} (helpers
+    // use no stages)
+    double2* hpart = reinterpret_cast<double2*>(smem + ((C::kPK * 16 + 127) & ~(size_t)127));
+    static_assert(((C::kPK * 16 + 127) & ~(size_t)127) + (size_t)C::kFarWarps * B * 16 <= C::kStageRegion,
+                  "helper partials fit the stage region");
     const int yi = tid / C::kYP, yp = tid % C::kYP;               // D^{-1} product: row, column class
     int hit = 0;                                                   // blocks done by this CTA
     for (int k = blockIdx.x - C::kCluster; k < nblk; k += H, hit++) {
@@ -789,62 +801,61 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
             mbar_expect_tx(full, (uint32_t)(C::kPK * 16));
             bulk_g2s(smem, a.dinv + (int64_t)k * C::kPK, C::kPK * 16, full);
         }
-        double2 acc[C::kRPW];
-        int64_t* wp = sRowP + warp * C::kRPW;
-        int32_t* wl = sRowL + warp * C::kRPW;
-        if (lane < C::kRPW) {
-            const int64_t i = row0 + warp * C::kRPW + lane;
+        if (warp == 0) {
+            const int64_t i = row0 + lane;
             int64_t p0 = 0, l0 = 0;
             if (i < n) {
                 p0 = a.farptr[i];
                 l0 = a.farptr[i + 1] - p0;
             }
-            wp[lane] = p0;
-            wl[lane] = (int32_t)l0;
+            sRowP[lane] = p0;
+            sRowL[lane] = (int32_t)l0;
         }
-        __syncwarp();
-        int nch = 0;
-#pragma unroll
-        for (int r = 0; r < C::kRPW; r++) {
-            acc[r] = make_double2(0.0, 0.0);
-            nch = max(nch, (wl[r] + 31) >> 5);
-        }
-        // chunk c of every owned row before chunk c+1 of any (oldest sources first): issue
-        // the column/value loads of all rows, wait once for the chunk's newest source
-        // block, then gather x kGrp rows at a time
+        hpart[warp * B + lane] = make_double2(0.0, 0.0);
+        const int64_t t0 = __ldg(a.itemptr + k), t1 = __ldg(a.itemptr + k + 1);
+        bar_named(1, C::kHelperT);
 #pragma unroll 1
-        for (int c = 0; c < nch; c++) {
-            const int32_t t = c * 32 + lane;
-            int32_t cc[C::kRPW];
-            double2 vv[C::kRPW];
+        for (int64_t t = t0 + warp; t < t1; t += (int64_t)C::kFarWarps * kHU) {
+            int32_t cc[kHU];
+            double2 vv[kHU];
+            int rr[kHU];
             int32_t need = -1;
 #pragma unroll
-            for (int r = 0; r < C::kRPW; r++) {
-                cc[r] = -1;
-                if (t < wl[r]) {
-                    cc[r] = ld_stream(a.fcol + wp[r] + t);
-                    vv[r] = ld_stream2(a.fval + wp[r] + t);
-                    need = max(need, cc[r]);
+            for (int u = 0; u < kHU; u++) {
+                const int64_t tt = t + (int64_t)u * C::kFarWarps;
+                const uint32_t it = tt < t1 ? __ldg(a.items + tt) : 0xffffffffu;
+                rr[u] = it == 0xffffffffu ? -1 : (int)(it & (B - 1));
+                cc[u] = -1;
+                if (rr[u] >= 0) {
+                    const int32_t pos = (int32_t)(it >> 5) * 32 + lane;
+                    if (pos < sRowL[rr[u]]) {
+                        cc[u] = ld_stream(a.fcol + sRowP[rr[u]] + pos);
+                        vv[u] = ld_stream2(a.fval + sRowP[rr[u]] + pos);
+                        need = max(need, cc[u]);
+                    }
                 }
             }
             need = __reduce_max_sync(0xffffffffu, need);
             if (need >= 0) helper_wait(need / B + 1, sF, sLock, a.xfront, epoch);
+            double2 xv[kHU];
 #pragma unroll
-            for (int g = 0; g < C::kRPW; g += C::kGrp) {
-                double2 xv[C::kGrp];
+            for (int u = 0; u < kHU; u++)
+                if (cc[u] >= 0) xv[u] = ld_cg2(x + phys(cc[u]));
 #pragma unroll
-                for (int r = 0; r < C::kGrp; r++)
-                    if (cc[g + r] >= 0) xv[r] = ld_cg2(x + phys(cc[g + r]));
-#pragma unroll
-                for (int r = 0; r < C::kGrp; r++)
-                    if (cc[g + r] >= 0) acc[g + r] = cfma(acc[g + r], vv[g + r], xv[r]);
+            for (int u = 0; u < kHU; u++) {
+                double2 acc = make_double2(0.0, 0.0);
+                if (cc[u] >= 0) acc = cfma(acc, vv[u], xv[u]);
+                acc = warp_sum2(acc);
+                if (lane == 0 && rr[u] >= 0) hpart[warp * B + rr[u]] = cadd(hpart[warp * B + rr[u]], acc);
             }
         }
+        bar_named(1, C::kHelperT);
+        if (warp == 0) {   // lane = row: the 16 warp partials in order
+            double2 sm = hpart[lane];
 #pragma unroll
-        for (int r = 0; r < C::kRPW; r++) {
-            const double2 sm = warp_sum2(acc[r]);
-            const int64_t i = row0 + warp * C::kRPW + r;
-            if (lane == 0) sRf[warp * C::kRPW + r] = (i < n) ? csub(__ldg(bvec + phys(i)), sm) : make_double2(0.0, 0.0);
+            for (int w = 1; w < C::kFarWarps; w++) sm = cadd(sm, hpart[w * B + lane]);
+            const int64_t i = row0 + lane;
+            sRf[lane] = (i < n) ? csub(__ldg(bvec + phys(i)), sm) : make_double2(0.0, 0.0);
         }
         bar_named(1, C::kHelperT);
         mbar_wait(full, (uint32_t)(hit & 1));

@@ -41,6 +41,23 @@ def main():
                 ce = float(s.precond(e, 2).abs().max())
                 s.solve()
                 i = s.solve_info
+                # device ms of one L / U substitution and one SpMV (roofline evidence)
+                kms = {}
+                y = torch.empty_like(e)
+                for nm, fn in (("trsv_lower", lambda: pb.ss_precond(s.handle, 0 | 4, e.data_ptr(), y.data_ptr())),
+                               ("trsv_upper", lambda: pb.ss_precond(s.handle, 1 | 4, e.data_ptr(), y.data_ptr())),
+                               ("spmv", lambda: s.spmv(e))):
+                    fn()
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record()
+                    for _ in range(3):
+                        fn()
+                    b.record()
+                    b.synchronize()
+                    kms[nm] = a.elapsed_time(b) / 3
+                out["kernel_ms"] = kms
+                out["nnz_L"], out["nnz_U"] = s.setup_info["nnz_L"], s.setup_info["nnz_U"]
+                out["n"], out["nnz"] = s.n, s.build_info["nnz"]
                 out.update(setup_s=round(t1 - t0, 2), fill=round(s.setup_info["fill"], 2),
                            swaps=s.setup_info["pivot_swaps"], repaired=s.setup_info["pivots_repaired"],
                            condest=ce, iterations=i["iterations"], converged=i["converged"],
