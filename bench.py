@@ -430,6 +430,26 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
+def sweep_roofline(pinfo, ms_step, world):
+    """configs[4]: algorithmic bytes of every Arnoldi step of every solve of the sweep (SpMV +
+    M^-1 + CGS2, solve_bytes) over (a) the summed per-point solve times -- the average
+    bandwidth of one point's solve, which shares the GPU with the concurrent points -- and (b)
+    the sweep step (setup included: the whole-job rate).  Rank 0's points only."""
+    peak, src = peaks()
+    tot_b = tot_ms = 0.0
+    for r in pinfo:
+        si = {"nnz_L": r["nnz_L"], "nnz_U": r["nnz_U"]}
+        tot_b += solve_bytes(si, {"n": r["n"], "nnz": r["nnz"]}, r["iterations"], r["restart"])
+        tot_ms += r["solve_ms"]
+    ach = tot_b / (tot_ms * 1e-3) / 1e9 if tot_ms else None
+    return {"bound": "hbm", "kernel": "whole Arnoldi steps of each point's solve (SpMV + M^-1 + CGS2)",
+            "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak if ach else None,
+            "peak_source": src, "traffic": None, "points_rank0": len(pinfo), "bytes_rank0": tot_b,
+            "solve_ms_sum_rank0": tot_ms,
+            "achieved_over_step": tot_b * world / (ms_step * 1e-3) / 1e9 if ms_step else None,
+            "note": "per-point solve bandwidth; the sweep step itself is bound by the host iLUTP setups"}
+
+
 def run_sweep_bench(args):
     """configs[4]: the 64-point detuning sweep through sweep.run_sweep.  A step is the whole
     sweep: every rank builds, sets up and solves its contiguous shard, one Liouvillian at a
@@ -459,7 +479,8 @@ def run_sweep_bench(args):
     rec = {"solve_ms": 0.0, "iterations": 0, "points": 0}
     lock = threading.Lock()
     conc = max(1, min(args.concurrent, 8))
-    inner = concurrent_solver(conc)
+    pinfo: list = []
+    inner = concurrent_solver(conc, info=pinfo)
 
     def solve(p):
         row = inner(p)
@@ -472,6 +493,7 @@ def run_sweep_bench(args):
     for _ in range(args.warmup):   # warm-up: one point of the rank's shard (context, kernels, allocator)
         solve(points[shard_range(len(points), rank, world).start])
     rec.update(solve_ms=0.0, iterations=0, points=0)
+    pinfo.clear()
     clocks = ClockSampler(local)
     clocks.start()
     launches0 = pb.ss_kernel_launches()
@@ -513,6 +535,7 @@ def run_sweep_bench(args):
                        "concurrent_per_gpu": conc,
                        "l2": "inputs (factors of every point) larger than L2"},
             "converged": conv, "points": len(points),
+            "roofline": sweep_roofline(pinfo, ms_max / args.steps, world),
             "concurrent_per_gpu": conc,
             "gmres_iterations_per_s_per_point": its_sum / (solve_ms_sum * 1e-3) if solve_ms_sum else None,
             "solve_s_sum": solve_ms_sum * 1e-3,

@@ -96,7 +96,10 @@ struct HostCSR {
 //   d = 1 .. kDense  -> dense G_d = D_k^{-1} T_{k,k-d} (the chain teams)
 //   kDense < d < Q_k -> list B, staged per lieutenant CTA and block
 //   d >= Q_k         -> far part (helper CTAs)
-constexpr int kDense = 2;
+#ifndef SSB_KDENSE
+#define SSB_KDENSE 2   // (build-time experiment knob: 3 moves d = 3 from the lieutenants to the chain teams)
+#endif
+constexpr int kDense = SSB_KDENSE;
 constexpr int near_cap_b(int B) { return B <= 32 ? 1024 : 1024; }   // per lieutenant and block
 constexpr int kLieutenants = 7;   // list B CTAs of a chain cluster (trsv.cu; cluster = 1 + 7)
 constexpr int lt_rows(int B) { return (B + kLieutenants - 1) / kLieutenants; }   // rows per lieutenant

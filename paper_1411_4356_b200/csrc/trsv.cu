@@ -144,6 +144,13 @@ constexpr int kTrace = SS_TRACE_STAMPS;   // stamps per block when tracing (incl
 #define TPROF(k, i) ((void)0)
 #define LPROF(k, i) ((void)0)
 #endif
+#ifndef SSB_G3_WARPS
+#define SSB_G3_WARPS 0   // with kDense = 3: G3_k x_{k-3} by the chain CTA's two idle warps (3, 4)
+#endif
+constexpr bool kG3Warps = SSB_G3_WARPS != 0;
+#ifndef SSB_PUSH_SPLIT
+#define SSB_PUSH_SPLIT 0   // lieutenants 0 .. SSB_PUSH_SPLIT-1 get x_k from team warp 0 (the rest from warp 1)
+#endif
 constexpr int kProducerSleep = 32;   // back-off of the producer polling a helper flag (ns)
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
@@ -211,7 +218,7 @@ struct Cfg {
     static constexpr int kRowsL = lt_rows(B);         // rows of a block per lieutenant
     static constexpr size_t kOffBinv = kOffBloc + (size_t)kNloc * 4;   // D_k^{-1} (packed; shared in L2 by all)
     static constexpr size_t kLtStage = kOffBinv + (size_t)kPK * 16;
-    static constexpr int kLtStages = 6;
+    static constexpr int kLtStages = kG3Warps ? 5 : 6;   // (the G3-warps variant needs 3 KB more)
     static constexpr size_t kOffLtRing = kLtStage * kLtStages;   // lieutenants' x ring
     static constexpr size_t kOffLtP = kOffLtRing + (size_t)kRingLt * B * 16;   // [kLtTeams][B] row partials
     static constexpr size_t kLtRegion = kOffLtP + (size_t)kLtTeams * B * 16;
@@ -223,7 +230,9 @@ struct Cfg {
     static constexpr size_t kOffXw = kOffTpart + (size_t)4 * kTeam * B * 16;   // [kTeams kTeam][B] own x_k
     static constexpr size_t kOffRowP = kOffXw + (size_t)kTeams * kTeam * B * 16;
     static constexpr size_t kOffRowL = kOffRowP + (size_t)B * 8;
-    static constexpr size_t kOffBar = kOffRowL + (size_t)B * 4;
+    static constexpr size_t kOffG3v = kOffRowL + (size_t)B * 4;                 // [4][B] G3_k x_{k-3}
+    static constexpr size_t kOffG3p = kOffG3v + (kG3Warps ? (size_t)4 * B * 16 : 0);   // [2][B] its halves
+    static constexpr size_t kOffBar = kOffG3p + (kG3Warps ? (size_t)2 * B * 16 : 0);
     // mbarriers: full/empty per S stage (lieutenants: per list B stage), full/empty per G
     // stage, xbar (lieutenant: x block landed), pbar (chain: partials landed), xfull (ring slot
     // holds x_k), pready (team partials), rfull (y_k staged), then int counters
@@ -237,9 +246,12 @@ struct Cfg {
     static constexpr size_t kOffXfull = kOffPbar + 8 * kPbuf;
     static constexpr size_t kOffPready = kOffXfull + 8 * kRing;
     static constexpr size_t kOffRfull = kOffPready + 8 * 4;
-    static constexpr size_t kOffInts = kOffRfull + 8 * kSStages;
+    static constexpr size_t kOffG3full = kOffRfull + 8 * kSStages;             // [4] G3 vector of block k ready
+    static constexpr size_t kOffInts = kOffG3full + (kG3Warps ? 8 * 4 : 0);
     static constexpr size_t kSmem = kOffInts + 64;
     static_assert(B == 32 && (kDense == 2 || kDense == 3), "the chain teams hold one row per lane, G1 .. G_kDense");
+    static_assert(!kG3Warps || kDense == 3, "the G3 warps need G3 (kDense = 3)");
+    static constexpr int kWG3 = 3;                    // G3 warps: 3, 4 (idle otherwise)
     static_assert(kCompute % B == 0 && B % kFarWarps == 0 && kRPW % kGrp == 0 && kFarWarps * 32 <= kNT, "layout");
     static constexpr int kHelperT = kFarWarps * 32;   // helper threads
     static constexpr int kYP = kHelperT / B;          // helper D^{-1} product: threads per row
@@ -383,12 +395,14 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
         for (int s = 0; s < C::kSStages; s++) mbar_init(rfull + s, 1);
         for (int s = 0; s < C::kGStages; s++) {
             mbar_init(gfull + s, 1);
-            mbar_init(gempty + s, C::kTeam);   // the warps of the team of block k
+            mbar_init(gempty + s, C::kTeam + (kG3Warps ? 2 : 0));   // the team of block k (+ the G3 warps)
         }
         for (int j = 0; j < C::kRingLt; j++) mbar_init(xbar + j, 1);
         for (int j = 0; j < C::kPbuf; j++) mbar_init(pbar + j, 1);
         for (int j = 0; j < C::kRing; j++) mbar_init(xfull + j, 32);   // the 32 lanes of the storing warp
         for (int j = 0; j < 4; j++) mbar_init(pready + j, C::kTeam * 32);   // every lane of a team
+        if (kG3Warps)
+            for (int j = 0; j < 4; j++) mbar_init(reinterpret_cast<uint64_t*>(smem + C::kOffG3full) + j, 32);
         *sF = 0;
         *sLock = 0;
         *sPub = 0;
@@ -536,7 +550,14 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     for (int u = 0; u < C::kSlice; u++) g1[u] = G[(j0 + u) * B + lane];
                     TPROF(k, 10);
                     double2 c1 = make_double2(0.0, 0.0);
-                    if constexpr (kDense >= 3) {
+                    if constexpr (kG3Warps) {
+                        // G3_k x_{k-3} from the G3 warps: warp 0 of the team adds it (once)
+                        if (tw == 0 && k >= 3) {
+                            mbar_wait(reinterpret_cast<uint64_t*>(smem + C::kOffG3full) + ((k - 3) & 3),
+                                      (uint32_t)(((k - 3) >> 2) & 1));
+                            c1 = reinterpret_cast<const double2*>(smem + C::kOffG3v)[((k - 3) & 3) * B + lane];
+                        }
+                    } else if constexpr (kDense >= 3) {
                         if (k >= 3) {   // x_{k-3}: this team's previous block
 #pragma unroll
                             for (int u = 0; u < C::kSlice; u++)
@@ -597,10 +618,12 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                 TPROF(k, 3);
                 // only warps 0 (ring) and 1 (lieutenants) need x_k (and, with kDense >= 3, every
                 // warp for its x_{k-3} carry): the others go on to their next block
-                if (kDense < 3 && tw >= 2) continue;
+                if ((kDense < 3 || kG3Warps) && tw >= 2) continue;
                 // y_k - sum_l q_l (the lieutenants' D_k^{-1}-multiplied partials), overlapping the
                 // other warps' partials
+#if !defined(SSB_NO_Q_WAIT)   // (timing experiment only: the chain without the q wait; wrong results)
                 mbar_wait(pbar + k % C::kPbuf, (uint32_t)((k / C::kPbuf) & 1));
+#endif
                 if (trace && tw == 0 && lane == 0) STAMP(k, 6);
 #pragma unroll
                 for (int l = 0; l < C::kLt; l++) yk = csub(yk, pbuf[((k % C::kPbuf) * C::kLt + l) * B + lane]);
@@ -612,28 +635,67 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                 for (int w = 1; w < C::kTeam; w++) sum = cadd(sum, tpart[(pq * C::kTeam + w) * B + lane]);
                 const double2 xk = csub(yk, sum);
                 TPROF(k, 5);
+                // x_k to the lieutenants' rings (st.async completes 16 bytes of the peer's xbar):
+                // warp 1 pushes to lieutenants [kPush0, kLt), warp 0 -- after releasing x_k in
+                // the local ring for the next team -- to [0, kPush0)
+                constexpr int kPush0 = SSB_PUSH_SPLIT;
+                auto push = [&](int l0, int l1) {
+                    const uint32_t off = (uint32_t)((((int64_t)k * B + lane) & (C::kRingLt * B - 1)) * 16);
+                    const uint32_t bar = (uint32_t)((k % C::kRingLt) * 8);
+#pragma unroll
+                    for (int l = l0; l < l1; l++) {
+                        if (lane == 0)   // the single arrival of the phase, expecting the block's bytes
+                            mbar_arrive_expect_tx_remote(peer_xbar[l] + bar, B * 16);
+                        st_async2(peer_ring[l] + off, xk, peer_xbar[l] + bar);
+                    }
+                };
                 if (tw == 0) {
                     ring[((int64_t)k * B + lane) & kRingMask] = xk;
                     mbar_arrive(xfull + k % C::kRing);   // every lane releases its own x_k[lane]
                     TPROF(k, 6);
                     if (trace && lane == 0) STAMP(k, 3);
+                    if constexpr (kPush0 > 0) push(0, kPush0);
                 } else if (tw == 1) {
-                    // x_k to every lieutenant's ring (st.async completes 16 bytes of its xbar)
-                    const uint32_t off = (uint32_t)((((int64_t)k * B + lane) & (C::kRingLt * B - 1)) * 16);
-                    const uint32_t bar = (uint32_t)((k % C::kRingLt) * 8);
-#pragma unroll
-                    for (int l = 0; l < C::kLt; l++) {
-                        if (lane == 0)   // the single arrival of the phase, expecting the block's bytes
-                            mbar_arrive_expect_tx_remote(peer_xbar[l] + bar, B * 16);
-                        st_async2(peer_ring[l] + off, xk, peer_xbar[l] + bar);
-                    }
+                    push(kPush0, C::kLt);
                     if (trace && lane == 0) STAMP(k, 8);
                 }
-                if constexpr (kDense >= 3) {
+                if constexpr (kDense >= 3 && !kG3Warps) {
                     xw[lane] = xk;   // my x_k: the carry of block k+3
                     __syncwarp();
                 }
                 TPROF(k, 7);
+            }
+        } else if (kG3Warps && chain && (warp == C::kWG3 || warp == C::kWG3 + 1)) {
+            // ------------------------------------------------ G3 warps: G3_k x_{k-3} (dense, from the
+            // G ring) as soon as x_{k-3} is in the ring, two halves of 16 columns, for the team
+            // of block k (two steps of slack: off the chain and off the lieutenants' DSMEM path)
+            const int h = warp - C::kWG3;
+            double2* g3p = reinterpret_cast<double2*>(smem + C::kOffG3p);
+            double2* g3v = reinterpret_cast<double2*>(smem + C::kOffG3v);
+            uint64_t* g3full = reinterpret_cast<uint64_t*>(smem + C::kOffG3full);
+            for (int k = 0; k < nblk; k++) {
+                const int s = k % C::kGStages;
+                mbar_wait(gfull + s, (uint32_t)((k / C::kGStages) & 1));
+                if (k >= 3) {
+                    const double2* G = reinterpret_cast<const double2*>(smem + C::kGStage * s) + 2 * B * B;
+                    mbar_wait(xfull + (k - 3) % C::kRing, (uint32_t)(((k - 3) / C::kRing) & 1));   // x_{k-3}
+                    const double2* x3 = ring + (((int64_t)(k - 3) * B) & kRingMask);
+                    double2 a0 = make_double2(0.0, 0.0), a1 = a0;
+#pragma unroll
+                    for (int u = 0; u < 16; u += 2) {
+                        a0 = cfma(a0, G[(h * 16 + u) * B + lane], x3[h * 16 + u]);
+                        a1 = cfma(a1, G[(h * 16 + u + 1) * B + lane], x3[h * 16 + u + 1]);
+                    }
+                    g3p[h * B + lane] = cadd(a0, a1);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(gempty + s);
+                bar_named(8, 64);   // both halves written
+                if (h == 0 && k >= 3) {
+                    g3v[((k - 3) & 3) * B + lane] = cadd(g3p[lane], g3p[B + lane]);
+                    mbar_arrive(g3full + ((k - 3) & 3));
+                }
+                bar_named(8, 64);   // halves read before the next block overwrites them
             }
         } else if (!chain) {
             // ------------------------------------------------ lieutenants: list B partial sums

@@ -29,7 +29,7 @@ def shard_range(npoints: int, rank: int, world: int) -> range:
     return range(lo, hi)
 
 
-def solve_point_gpu(p, concurrent: int = 1, host_threads: int = 0, stream=None) -> tuple:
+def solve_point_gpu(p, concurrent: int = 1, host_threads: int = 0, stream=None, info: list | None = None) -> tuple:
     """Build -> setup -> solve -> expect one parameter point on the current CUDA device.
 
     concurrent > 1: this point shares the GPU with concurrent - 1 others solved from other
@@ -46,12 +46,16 @@ def solve_point_gpu(p, concurrent: int = 1, host_threads: int = 0, stream=None) 
         s.solve()
         na, nb = s.expect()
         i = s.solve_info
+        if info is not None:   # (list.append is atomic: safe from several host threads)
+            info.append({"Delta": p.Delta, "n": s.n, "nnz": s.build_info["nnz"], "nnz_L": s.setup_info["nnz_L"],
+                         "nnz_U": s.setup_info["nnz_U"], "iterations": i["iterations"], "restart": p.restart,
+                         "solve_ms": i["solve_ms"]})
         return (p.Delta, na, nb, i["iterations"], i["rel_residual"], i["converged"], i["solve_ms"])
     finally:
         s.close()
 
 
-def concurrent_solver(concurrent: int, host_cores: int | None = None) -> Callable:
+def concurrent_solver(concurrent: int, host_cores: int | None = None, info: list | None = None) -> Callable:
     """A solve(p) for run_sweep that may be called from `concurrent` host threads at once:
     each call on the calling thread's own CUDA stream (same device as the caller of
     run_sweep), with 1/concurrent of the GPU's co-resident clusters for its substitutions
@@ -69,7 +73,7 @@ def concurrent_solver(concurrent: int, host_cores: int | None = None) -> Callabl
         torch.cuda.set_device(dev)
         if not hasattr(local, "stream"):
             local.stream = torch.cuda.Stream(device=dev)
-        return solve_point_gpu(p, concurrent, max(1, cores // concurrent), local.stream)
+        return solve_point_gpu(p, concurrent, max(1, cores // concurrent), local.stream, info)
 
     return solve
 

@@ -73,6 +73,16 @@ def main():
             d["slow_team_reduced_ns"] = med((rel[:, 0] - done_prev)[slow])
             d["slow_lt_late_landed_ns"] = med((rel[:, 7] - done_prev)[slow])
             d["slow_producer_flag_ns"] = med((rel[:, 5] - done_prev)[slow])
+            d["slow_team_q_landed_ns"] = med((rel[:, 6] - done_prev)[slow])
+            d["slow_lt_q_sent_ns"] = med((rel[:, 9] - done_prev)[slow])
+            d["slow_lt6_q_sent_ns"] = med((rel[:, 2] - done_prev)[slow])
+            d["slow_lt_early_done_ns"] = med((rel[:, 11] - done_prev)[slow])
+            d["slow_lt_stage_ready_ns"] = med((rel[:, 12] - done_prev)[slow])
+            # where the excess goes: steps whose y_k flag came late vs. whose q came late
+            late_y = (rel[:, 5] - done_prev) > -500
+            late_q = (rel[:, 6] - done_prev) > 350
+            d["excess_late_y_us"] = float(ex[late_y].sum() / 1e3)
+            d["excess_late_q_not_y_us"] = float(ex[late_q & ~late_y].sum() / 1e3)
         out[nm] = d
     print(json.dumps(out), flush=True)
     s.close()
