@@ -100,7 +100,10 @@ struct HostCSR {
 #define SSB_KDENSE 2   // (build-time experiment knob: 3 moves d = 3 from the lieutenants to the chain teams)
 #endif
 constexpr int kDense = SSB_KDENSE;
-constexpr int near_cap_b(int B) { return B <= 32 ? 1024 : 1024; }   // per lieutenant and block
+#ifndef SSB_LTCAP
+#define SSB_LTCAP 1024   // list-B entries per lieutenant and block (the lieutenants' shared-memory stage)
+#endif
+constexpr int near_cap_b(int B) { return B > 0 ? SSB_LTCAP : SSB_LTCAP; }   // per lieutenant and block
 constexpr int kLieutenants = 7;   // list B CTAs of a chain cluster (trsv.cu; cluster = 1 + 7)
 constexpr int lt_rows(int B) { return (B + kLieutenants - 1) / kLieutenants; }   // rows per lieutenant
 constexpr int near_nloc(int B) { return 2 * (B + 4); }   // per list: row starts | late-part starts

@@ -144,6 +144,10 @@ constexpr int kTrace = SS_TRACE_STAMPS;   // stamps per block when tracing (incl
 #define TPROF(k, i) ((void)0)
 #define LPROF(k, i) ((void)0)
 #endif
+#ifndef SSB_LT_DINV_LDG
+#define SSB_LT_DINV_LDG 0   // lieutenants read their columns of D_k^{-1} from global memory (L2), not staged
+#endif
+constexpr bool kLtDinvLdg = SSB_LT_DINV_LDG != 0;
 #ifndef SSB_G3_WARPS
 #define SSB_G3_WARPS 0   // with kDense = 3: G3_k x_{k-3} by the chain CTA's two idle warps (3, 4)
 #endif
@@ -217,7 +221,7 @@ struct Cfg {
     static constexpr size_t kOffBloc = kOffBval + (size_t)kCapB * 16;
     static constexpr int kRowsL = lt_rows(B);         // rows of a block per lieutenant
     static constexpr size_t kOffBinv = kOffBloc + (size_t)kNloc * 4;   // D_k^{-1} (packed; shared in L2 by all)
-    static constexpr size_t kLtStage = kOffBinv + (size_t)kPK * 16;
+    static constexpr size_t kLtStage = kOffBinv + (kLtDinvLdg ? 0 : (size_t)kPK * 16);
     static constexpr int kLtStages = kG3Warps ? 5 : 6;   // (the G3-warps variant needs 3 KB more)
     static constexpr size_t kOffLtRing = kLtStage * kLtStages;   // lieutenants' x ring
     static constexpr size_t kOffLtP = kOffLtRing + (size_t)kRingLt * B * 16;   // [kLtTeams][B] row partials
@@ -462,10 +466,10 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     unsigned char* st = sbase + stsz * s;
                     const int g = k * C::kLt + (role - 1);   // this lieutenant's rows of block k
                     stage_near(st + C::kOffBcol, st + C::kOffBval, st + C::kOffBloc, b0, b1, a.ncolB, a.nvalB,
-                               a.nlocB, g, C::kNloc, full + s, (uint32_t)(C::kPK * 16));
+                               a.nlocB, g, C::kNloc, full + s, kLtDinvLdg ? 0u : (uint32_t)(C::kPK * 16));
                     // the whole packed D_k^{-1}: the helper and all seven lieutenants read the same
                     // 8.4 KB, so DRAM sees it once (L2)
-                    bulk_g2s(st + C::kOffBinv, a.dinv + (int64_t)k * C::kPK, C::kPK * 16, full + s);
+                    if (!kLtDinvLdg) bulk_g2s(st + C::kOffBinv, a.dinv + (int64_t)k * C::kPK, C::kPK * 16, full + s);
                 }
             }
         } else if (chain && warp == C::kWGProducer) {
@@ -723,6 +727,19 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                 for (int k = lteam; k < nblk; k += C::kLtTeams) {
                     const int s = k % nst;
                     unsigned char* st = smem + stsz * s;
+                    constexpr int kRows = C::kRowsL;
+                    double2 dq[kRows];   // D_k^{-1}[tt, l + kLt m] (predicated: 0 above the diagonal)
+                    if (kLtDinvLdg && tt < B) {   // from L2 (the helper of block k staged it long ago)
+                        const double2* gInv = a.dinv + (int64_t)k * C::kPK;
+#pragma unroll
+                        for (int m = 0; m < kRows; m++) {
+                            const int rr = m * C::kLt + l;
+                            const bool ok = rr <= tt;
+                            dq[m] = __ldg(gInv + (ok ? rr * B - (rr * (rr - 1)) / 2 + (tt - rr) : 0));
+                            dq[m].x = ok ? dq[m].x : 0.0;
+                            dq[m].y = ok ? dq[m].y : 0.0;
+                        }
+                    }
                     LPROF(k, 0);
                     mbar_wait(full + s, (uint32_t)((k / nst) & 1));
                     LPROF(k, 1);
@@ -761,9 +778,7 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     };
                     if (rowok && q < C::kTPRlate) pre(lt0, lt1, lc0, lc1, lv0, lv1);
                     // and this thread's entries of D_k^{-1} for the q product below
-                    constexpr int kRows = C::kRowsL;
-                    double2 dq[kRows];   // D_k^{-1}[tt, l + kLt m] (predicated: 0 above the diagonal)
-                    if (tt < B) {
+                    if (!kLtDinvLdg && tt < B) {
                         const double2* sInv = reinterpret_cast<const double2*>(st + C::kOffBinv);
 #pragma unroll
                         for (int m = 0; m < kRows; m++) {

@@ -38,9 +38,21 @@ def main():
                 s.solve()
             i = s.solve_info
             na, nb = s.expect()
-            e = torch.ones(s.n, dtype=torch.complex128, device="cuda")
-            return dict(Delta=p.Delta, it=i["iterations"], conv=i["converged"], res=i["rel_residual"], na=na, nb=nb,
-                        nnzL=s.setup_info["nnz_L"], nnzU=s.setup_info["nnz_U"], swaps=s.setup_info["pivot_swaps"])
+            out = dict(Delta=p.Delta, it=i["iterations"], conv=i["converged"], res=i["rel_residual"], na=na, nb=nb,
+                       nnzL=s.setup_info["nnz_L"], nnzU=s.setup_info["nnz_U"], swaps=s.setup_info["pivot_swaps"])
+            if i["converged"] != 1:
+                # transient (the launch) or persistent (the data on the device)?  M^{-1} e twice, then
+                # the solve again, on the same handle, with nothing else running in this thread
+                torch.cuda.synchronize()
+                e = torch.ones(s.n, dtype=torch.complex128, device="cuda")
+                e1, e2 = e.clone(), e.clone()
+                torch.cuda.synchronize()
+                y1, y2 = s.precond(e1), s.precond(e2)
+                out["again_precond_finite"] = [bool(torch.isfinite(torch.view_as_real(y)).all()) for y in (y1, y2)]
+                out["again_precond_equal"] = bool(torch.equal(y1, y2))
+                s.solve()
+                out["again_solve"] = [s.solve_info["iterations"], s.solve_info["converged"]]
+            return out
         finally:
             s.close()
 
