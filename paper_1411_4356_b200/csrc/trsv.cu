@@ -152,6 +152,10 @@ constexpr bool kLtDinvLdg = SSB_LT_DINV_LDG != 0;
 #define SSB_G3_WARPS 0   // with kDense = 3: G3_k x_{k-3} by the chain CTA's two idle warps (3, 4)
 #endif
 constexpr bool kG3Warps = SSB_G3_WARPS != 0;
+#ifndef SSB_LT_GATE
+#define SSB_LT_GATE 0   // lieutenants: the early part of block k waits for block k-1's late part (1) or its q (2)
+#endif
+constexpr int kLtGate = SSB_LT_GATE;
 #ifndef SSB_PUSH_SPLIT
 #define SSB_PUSH_SPLIT 0   // lieutenants 0 .. SSB_PUSH_SPLIT-1 get x_k from team warp 0 (the rest from warp 1)
 #endif
@@ -252,6 +256,7 @@ struct Cfg {
     static constexpr size_t kOffRfull = kOffPready + 8 * 4;
     static constexpr size_t kOffG3full = kOffRfull + 8 * kSStages;             // [4] G3 vector of block k ready
     static constexpr size_t kOffInts = kOffG3full + (kG3Warps ? 8 * 4 : 0);
+    static constexpr size_t kOffLbar = kOffInts + 32;   // [4] (lieutenants) late part of block k done
     static constexpr size_t kSmem = kOffInts + 64;
     static_assert(B == 32 && (kDense == 2 || kDense == 3), "the chain teams hold one row per lane, G1 .. G_kDense");
     static_assert(!kG3Warps || kDense == 3, "the G3 warps need G3 (kDense = 3)");
@@ -405,6 +410,7 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
         for (int j = 0; j < C::kPbuf; j++) mbar_init(pbar + j, 1);
         for (int j = 0; j < C::kRing; j++) mbar_init(xfull + j, 32);   // the 32 lanes of the storing warp
         for (int j = 0; j < 4; j++) mbar_init(pready + j, C::kTeam * 32);   // every lane of a team
+        for (int j = 0; j < 4; j++) mbar_init(reinterpret_cast<uint64_t*>(smem + C::kOffLbar) + j, 1);
         if (kG3Warps)
             for (int j = 0; j < 4; j++) mbar_init(reinterpret_cast<uint64_t*>(smem + C::kOffG3full) + j, 32);
         *sF = 0;
@@ -711,6 +717,7 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
             // Each lieutenant sends q_l = D_k^{-1}[:, its rows] (its row partials), so the chain
             // only subtracts the three q_l from y_k = D_k^{-1} r_k.
             const int l = role - 1;
+            uint64_t* lbar = reinterpret_cast<uint64_t*>(smem + C::kOffLbar);
             const uint32_t peer_pbuf = mapa(smem_u32(pbuf), 0u);
             const uint32_t peer_pbar = mapa(smem_u32(pbar), 0u);
             const double2* ltring = reinterpret_cast<const double2*>(smem + C::kOffLtRing);
@@ -750,6 +757,9 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     const double2* val = reinterpret_cast<const double2*>(st + C::kOffBval);
                     double2 acc = make_double2(0.0, 0.0);
                     land(k - kDense - 2);
+                    if constexpr (kLtGate > 0) {   // block k-1's late part (same trigger x_{k-3}) first
+                        if (k >= 1) mbar_wait(lbar + ((k - 1) & 3), (uint32_t)(((k - 1) >> 2) & 1));
+                    }
                     LPROF(k, 2);
                     if (rowok) acc = near_range<B, C::kTPRl, C::kRingLt>(col, val, ltring, loc[r], loc[C::kLate + r], q, acc);
 #pragma unroll
@@ -808,6 +818,7 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     LPROF(k, 5);
                     if (rowok && q == 0) lp[r] = acc;
                     bar_named(2 + lteam, C::kLtTeamT);
+                    if (kLtGate == 1 && tt == 0) mbar_arrive(lbar + (k & 3));
                     LPROF(k, 6);
                     // q_l = D_k^{-1}[:, rows of l] p_l: one thread per output row i (the team's first
                     // warp), the lieutenant's rows rr = l, l + kLt, ... <= i in order
@@ -828,6 +839,10 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                         const int pk = k % C::kPbuf;
                         st_async2(peer_pbuf + (uint32_t)(((pk * C::kLt + l) * B + i) * 16), cadd(qa, qb),
                                   peer_pbar + (uint32_t)(pk * 8));
+                        if (kLtGate == 2) {
+                            __syncwarp();
+                            if (tt == 0) mbar_arrive(lbar + (k & 3));
+                        }
                         LPROF(k, 7);
                         if (tr0) STAMP(k, 9);
                         if (trace && tt == 0 && l == C::kLt - 1) STAMP(k, 2);
