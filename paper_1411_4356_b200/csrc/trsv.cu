@@ -156,6 +156,15 @@ constexpr bool kG3Warps = SSB_G3_WARPS != 0;
 #define SSB_LT_GATE 0   // lieutenants: the early part of block k waits for block k-1's late part (1) or its q (2)
 #endif
 constexpr int kLtGate = SSB_LT_GATE;
+#ifndef SSB_LT_G3
+#define SSB_LT_G3 0   // with kDense = 3: G3_k x_{k-3} by the lieutenants (columns l, l+7, ... of G3_k from L2), not the chain
+#endif
+constexpr bool kLtG3 = SSB_LT_G3 != 0;
+constexpr int kChainDense = kLtG3 ? 2 : kDense;   // dense blocks the chain teams apply (G ring stage)
+#ifndef SSB_ROWWARPS
+#define SSB_ROWWARPS 0   // chain teams: warp w owns ROWS 8w .. 8w+7 (4 lanes per row, shuffle reduction) instead of columns
+#endif
+constexpr bool kRowWarps = SSB_ROWWARPS != 0;
 #ifndef SSB_PUSH_SPLIT
 #define SSB_PUSH_SPLIT 0   // lieutenants 0 .. SSB_PUSH_SPLIT-1 get x_k from team warp 0 (the rest from warp 1)
 #endif
@@ -215,7 +224,7 @@ struct Cfg {
     static constexpr int kTPRlate = 4;                //              and of them for the late part
     // chain CTA: a G ring (G1_k | G2_k | G3_k) and an S ring (y_k), filled independently (G is
     // static, y_k waits for the helpers)
-    static constexpr size_t kGStage = (size_t)kDense * B * B * 16;
+    static constexpr size_t kGStage = (size_t)kChainDense * B * B * 16;
     static constexpr size_t kOffSR = kGStage * kGStages;
     static constexpr size_t kSStage = (size_t)B * 16;
     static constexpr size_t kChainRegion = kOffSR + kSStage * kSStages;
@@ -260,6 +269,7 @@ struct Cfg {
     static constexpr size_t kSmem = kOffInts + 64;
     static_assert(B == 32 && (kDense == 2 || kDense == 3), "the chain teams hold one row per lane, G1 .. G_kDense");
     static_assert(!kG3Warps || kDense == 3, "the G3 warps need G3 (kDense = 3)");
+    static_assert(!kLtG3 || (kDense == 3 && !kG3Warps), "lieutenant G3 needs G3 (kDense = 3)");
     static constexpr int kWG3 = 3;                    // G3 warps: 3, 4 (idle otherwise)
     static_assert(kCompute % B == 0 && B % kFarWarps == 0 && kRPW % kGrp == 0 && kFarWarps * 32 <= kNT, "layout");
     static constexpr int kHelperT = kFarWarps * 32;   // helper threads
@@ -541,6 +551,112 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                 peer_ring[l] = mapa(smem_u32(smem + C::kOffLtRing), (uint32_t)(l + 1));
                 peer_xbar[l] = mapa(smem_u32(xbar), (uint32_t)(l + 1));
             }
+            if constexpr (kRowWarps) {
+                // ---- row-owning variant: warp tw owns rows 8 tw .. 8 tw + 7, lane = (rr = lane & 7,
+                // g = lane >> 3) takes columns g, g + 4, ..., g + 28 of its row; the four lanes of a
+                // row reduce by shuffles (no partials in shared memory, no pready hand-off), lane
+                // group g also adds q_g and q_{g+4} and pushes x_k to those lieutenants.
+                static_assert(!kRowWarps || (kChainDense == 2 && B == 32 && C::kTeam == 4 && C::kLt <= 8), "row-owning teams");
+                const int rr = lane & 7, g = lane >> 3, r = tw * 8 + rr;
+                const int l0 = g, l1 = g + 4;   // this lane group's lieutenants (l1 only if < kLt)
+                const uint32_t pr0 = mapa(smem_u32(smem + C::kOffLtRing), (uint32_t)(l0 + 1));
+                const uint32_t pb0 = mapa(smem_u32(xbar), (uint32_t)(l0 + 1));
+                const uint32_t pr1 = mapa(smem_u32(smem + C::kOffLtRing), (uint32_t)((l1 < C::kLt ? l1 : l0) + 1));
+                const uint32_t pb1 = mapa(smem_u32(xbar), (uint32_t)((l1 < C::kLt ? l1 : l0) + 1));
+                for (int k = team; k < nblk; k += C::kTeams) {
+                    TPROF(k, 0);
+                    if (k >= C::kRing)   // ring slot of block k held block k-kRing: published?
+                        while (ld_acq_cta(sPub) < k - C::kRing + 1) {
+                        }
+                    TPROF(k, 8);
+                    double2 g1[8];
+                    double2 carry = make_double2(0.0, 0.0), carry2 = carry;
+                    {
+                        const int s = k % C::kGStages;
+                        mbar_wait(gfull + s, (uint32_t)((k / C::kGStages) & 1));
+                        TPROF(k, 9);
+                        const double2* G = reinterpret_cast<const double2*>(smem + C::kGStage * s);
+#pragma unroll
+                        for (int u = 0; u < 8; u++) g1[u] = G[(g + 4 * u) * B + r];
+                        TPROF(k, 10);
+                        if (k >= 2) {
+                            mbar_wait(xfull + (k - 2) % C::kRing, (uint32_t)(((k - 2) / C::kRing) & 1));   // x_{k-2}
+                            TPROF(k, 12);
+                            const double2* x2 = ring + (((int64_t)(k - 2) * B) & kRingMask);
+#pragma unroll
+                            for (int u = 0; u < 8; u += 2) {
+                                carry = cfma(carry, G[B * B + (g + 4 * u) * B + r], x2[g + 4 * u]);
+                                carry2 = cfma(carry2, G[B * B + (g + 4 * u + 4) * B + r], x2[g + 4 * u + 4]);
+                            }
+                        }
+                        carry = cadd(carry, carry2);
+                        TPROF(k, 13);
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(gempty + s);
+                    }
+                    double2 yk;
+                    {
+                        const int s = k % C::kSStages;
+                        mbar_wait(rfull + s, (uint32_t)((k / C::kSStages) & 1));
+                        yk = reinterpret_cast<const double2*>(smem + C::kOffSR + C::kSStage * s)[r];
+                        __syncwarp();
+                        if (lane == 0) {
+                            mbar_arrive(empty + s);
+                            if (tw == 0) mbar_expect_tx(pbar + k % C::kPbuf, (uint32_t)(C::kLt * B * 16));   // the q_l of block k
+                        }
+                    }
+                    TPROF(k, 1);
+                    if (trace && tw == 0 && lane == 0) STAMP(k, 10);
+                    // ---- the chain
+                    double2 p0 = carry, p1 = make_double2(0.0, 0.0);
+                    double2 p2 = make_double2(0.0, 0.0), p3 = make_double2(0.0, 0.0);
+                    if (k >= 1) {
+                        mbar_wait(xfull + (k - 1) % C::kRing, (uint32_t)(((k - 1) / C::kRing) & 1));   // x_{k-1}
+                        const double2* xr = ring + (((int64_t)(k - 1) * B) & kRingMask);
+                        TPROF(k, 2);
+                        if (trace && tw == 0 && lane == 0) STAMP(k, 13);
+#pragma unroll
+                        for (int u = 0; u < 8; u += 4) {
+                            p0 = cfma(p0, g1[u], xr[g + 4 * u]);
+                            p1 = cfma(p1, g1[u + 1], xr[g + 4 * u + 4]);
+                            p2 = cfma(p2, g1[u + 2], xr[g + 4 * u + 8]);
+                            p3 = cfma(p3, g1[u + 3], xr[g + 4 * u + 12]);
+                        }
+                    }
+                    double2 p = cadd(cadd(p0, p1), cadd(p2, p3));
+                    TPROF(k, 3);
+                    mbar_wait(pbar + k % C::kPbuf, (uint32_t)((k / C::kPbuf) & 1));   // the lieutenants' q_l
+                    if (trace && tw == 0 && lane == 0) STAMP(k, 6);
+                    p = cadd(p, pbuf[((k % C::kPbuf) * C::kLt + l0) * B + r]);
+                    if (l1 < C::kLt) p = cadd(p, pbuf[((k % C::kPbuf) * C::kLt + l1) * B + r]);
+                    TPROF(k, 4);
+                    p.x += __shfl_xor_sync(0xffffffffu, p.x, 8);
+                    p.y += __shfl_xor_sync(0xffffffffu, p.y, 8);
+                    p.x += __shfl_xor_sync(0xffffffffu, p.x, 16);
+                    p.y += __shfl_xor_sync(0xffffffffu, p.y, 16);
+                    const double2 xk = csub(yk, p);
+                    if (trace && tw == 0 && lane == 0) STAMP(k, 0);
+                    TPROF(k, 5);
+                    if (g == 0) {
+                        ring[((int64_t)k * B + r) & kRingMask] = xk;
+                        mbar_arrive(xfull + k % C::kRing);   // 8 lanes of each of the 4 warps: 32 arrivals
+                    }
+                    TPROF(k, 6);
+                    if (trace && tw == 0 && lane == 0) STAMP(k, 3);
+                    {
+                        const uint32_t off = (uint32_t)((((int64_t)k * B + r) & (C::kRingLt * B - 1)) * 16);
+                        const uint32_t bar = (uint32_t)((k % C::kRingLt) * 8);
+                        if (tw == 0 && rr == 0) {   // the single arrival of each lieutenant's phase
+                            mbar_arrive_expect_tx_remote(pb0 + bar, B * 16);
+                            if (l1 < C::kLt) mbar_arrive_expect_tx_remote(pb1 + bar, B * 16);
+                        }
+                        st_async2(pr0 + off, xk, pb0 + bar);
+                        if (l1 < C::kLt) st_async2(pr1 + off, xk, pb1 + bar);
+                    }
+                    if (trace && tw == 1 && lane == 0) STAMP(k, 8);
+                    TPROF(k, 7);
+                }
+            } else {
             for (int k = team; k < nblk; k += C::kTeams) {
                 const int pq = k & 3;
                 TPROF(k, 0);
@@ -567,7 +683,7 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                                       (uint32_t)(((k - 3) >> 2) & 1));
                             c1 = reinterpret_cast<const double2*>(smem + C::kOffG3v)[((k - 3) & 3) * B + lane];
                         }
-                    } else if constexpr (kDense >= 3) {
+                    } else if constexpr (kChainDense >= 3) {
                         if (k >= 3) {   // x_{k-3}: this team's previous block
 #pragma unroll
                             for (int u = 0; u < C::kSlice; u++)
@@ -628,7 +744,7 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                 TPROF(k, 3);
                 // only warps 0 (ring) and 1 (lieutenants) need x_k (and, with kDense >= 3, every
                 // warp for its x_{k-3} carry): the others go on to their next block
-                if ((kDense < 3 || kG3Warps) && tw >= 2) continue;
+                if ((kChainDense < 3 || kG3Warps) && tw >= 2) continue;
                 // y_k - sum_l q_l (the lieutenants' D_k^{-1}-multiplied partials), overlapping the
                 // other warps' partials
 #if !defined(SSB_NO_Q_WAIT)   // (timing experiment only: the chain without the q wait; wrong results)
@@ -669,11 +785,12 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     push(kPush0, C::kLt);
                     if (trace && lane == 0) STAMP(k, 8);
                 }
-                if constexpr (kDense >= 3 && !kG3Warps) {
+                if constexpr (kChainDense >= 3 && !kG3Warps) {
                     xw[lane] = xk;   // my x_k: the carry of block k+3
                     __syncwarp();
                 }
                 TPROF(k, 7);
+            }
             }
         } else if (kG3Warps && chain && (warp == C::kWG3 || warp == C::kWG3 + 1)) {
             // ------------------------------------------------ G3 warps: G3_k x_{k-3} (dense, from the
@@ -747,6 +864,15 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                             dq[m].y = ok ? dq[m].y : 0.0;
                         }
                     }
+                    double2 g3[kRows];   // (kLtG3) G3_k[tt, l + kLt m]: prefetched into L2 now, loaded below
+                    if (kLtG3 && tt < B && k >= 3) {
+                        const double2* gG3 = a.G + ((int64_t)k * kDense + 2) * B * B + tt;
+#pragma unroll
+                        for (int m = 0; m < kRows; m++) {
+                            const int c = m * C::kLt + l;
+                            if (c < B) asm volatile("prefetch.global.L2 [%0];" ::"l"(gG3 + c * B));
+                        }
+                    }
                     LPROF(k, 0);
                     mbar_wait(full + s, (uint32_t)((k / nst) & 1));
                     LPROF(k, 1);
@@ -799,6 +925,14 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                             dq[m].y = ok ? dq[m].y : 0.0;
                         }
                     }
+                    if (kLtG3 && tt < B && k >= 3) {   // (L2 hits: prefetched at the top of the block)
+                        const double2* gG3 = a.G + ((int64_t)k * kDense + 2) * B * B + tt;
+#pragma unroll
+                        for (int m = 0; m < kRows; m++) {
+                            const int c = m * C::kLt + l;
+                            g3[m] = c < B ? __ldg(gG3 + c * B) : make_double2(0.0, 0.0);
+                        }
+                    }
                     LPROF(k, 3);
                     if (tr0) STAMP(k, 11);
                     land(k - kDense - 1);
@@ -837,7 +971,21 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                             if (m + 1 < kRows) qb = cfma(qb, dq[m + 1], pq[m + 1]);
                         }
                         const int pk = k % C::kPbuf;
-                        st_async2(peer_pbuf + (uint32_t)(((pk * C::kLt + l) * B + i) * 16), cadd(qa, qb),
+                        double2 qv = cadd(qa, qb);
+                        if (kLtG3 && k >= 3) {   // + G3_k[:, my columns] x_{k-3}[my columns]: the only late term
+                            land(k - 3);
+                            if (tr0) STAMP(k, 14);
+                            const double2* x3 = ltring + (((int64_t)(k - 3) * B) & kRM);
+                            double2 qc = make_double2(0.0, 0.0);
+#pragma unroll
+                            for (int m = 0; m < kRows; m += 2) {
+                                const int c0 = m * C::kLt + l, c1 = (m + 1) * C::kLt + l;
+                                qv = cfma(qv, g3[m], x3[c0 < B ? c0 : 0]);
+                                if (m + 1 < kRows) qc = cfma(qc, g3[m + 1], x3[c1 < B ? c1 : 0]);
+                            }
+                            qv = cadd(qv, qc);
+                        }
+                        st_async2(peer_pbuf + (uint32_t)(((pk * C::kLt + l) * B + i) * 16), qv,
                                   peer_pbar + (uint32_t)(pk * 8));
                         if (kLtGate == 2) {
                             __syncwarp();
