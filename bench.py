@@ -533,6 +533,7 @@ def run_sweep_bench(args):
                        "restart": SWEEP_BASE.restart, "tol": SWEEP_BASE.tol, "ranks": world,
                        "sharding": "contiguous blocks of points per rank; observables all-gathered (NCCL)",
                        "concurrent_per_gpu": conc,
+                       "concurrency": "setups (host iLUTP) of concurrent_per_gpu points overlap; GMRES solves one at a time on the whole GPU",
                        "l2": "inputs (factors of every point) larger than L2"},
             "converged": conv, "points": len(points),
             "roofline": sweep_roofline(pinfo, ms_max / args.steps, world),

@@ -205,6 +205,14 @@ int ss_precond(ss_problem* h, int32_t which, const void* x_dev, void* y_dev);
 int ss_debug_trace_trsv(ss_problem* h, int32_t which, const void* x_dev, void* y_dev, uint64_t* host_trace,
                         int64_t* nblk_out);
 
+/* Test hook: fill the shared memory of every SM with 0xFF bytes (a NaN pattern as complex128) on
+ * the problem's stream.  Shared memory is not cleared between kernels, so this stands in for
+ * "whatever another kernel left there": a substitution that multiplies a zeroed value by a
+ * ring slot or partial it has not written in this launch (0 * NaN = NaN) fails after it
+ * (tests/test_gpu_parity.py::test_precond_ignores_stale_shared_memory).  Errors: SS_ERR_ARG,
+ * SS_ERR_CUDA. */
+int ss_debug_poison_smem(ss_problem* h);
+
 /* Limit the substitution kernels of this problem to `sms` SMs (rounded down to whole
  * 8-CTA clusters, at least 2 clusters; 0 = the whole GPU, the default), so that several
  * problems can run their solves concurrently on one GPU from different host threads and

@@ -13,12 +13,12 @@ from __future__ import annotations
 from . import _lib
 from ._lib import (SSError, ss_build, ss_setup, ss_solve, ss_expect, ss_get_rho, ss_solve_host,
                    ss_destroy, ss_sizes, ss_export_matrix, ss_export_perm, ss_export_colperm, ss_export_factors, ss_spmv,
-                   ss_precond, ss_kernel_launches, ss_debug_trace_trsv, ss_ilutp_host, ss_set_sm_budget)
+                   ss_precond, ss_kernel_launches, ss_debug_trace_trsv, ss_ilutp_host, ss_set_sm_budget, ss_debug_poison_smem)
 
 __all__ = ["SteadyState", "SSError", "ss_build", "ss_setup", "ss_solve", "ss_expect", "ss_get_rho",
            "ss_solve_host", "ss_destroy", "ss_sizes", "ss_export_matrix", "ss_export_perm", "ss_export_colperm",
            "ss_export_factors", "ss_spmv", "ss_precond", "ss_kernel_launches", "ss_debug_trace_trsv",
-           "ss_ilutp_host", "ss_set_sm_budget"]
+           "ss_ilutp_host", "ss_set_sm_budget", "ss_debug_poison_smem"]
 
 
 class SteadyState:

@@ -82,6 +82,7 @@ SIGNATURES = [
     ("ss_precond", ctypes.c_int, [P, I32, P, P]),
     ("ss_kernel_launches", ctypes.c_int64, []),
     ("ss_set_sm_budget", ctypes.c_int, [P, I32]),
+    ("ss_debug_poison_smem", ctypes.c_int, [P]),
     ("ss_debug_trace_trsv", ctypes.c_int, [P, I32, P, P, P, PI64]),
     ("ss_ilutp_host", ctypes.c_int, [ctypes.c_int64, P, P, P, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                      I32, P, P, P, ctypes.c_int64, P, P, P, ctypes.c_int64, P]),
@@ -138,6 +139,11 @@ def ss_export_colperm(h) -> np.ndarray:
     perm = np.empty(n, np.int64)
     _check(load().ss_export_colperm(h, perm.ctypes.data))
     return perm
+
+
+def ss_debug_poison_smem(h) -> None:
+    """Fill every SM's shared memory with a NaN pattern (test hook, include/ss_b200.h)."""
+    _check(load().ss_debug_poison_smem(h))
 
 
 def ss_set_sm_budget(h, sms: int) -> None:

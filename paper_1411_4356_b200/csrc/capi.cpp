@@ -159,6 +159,14 @@ int ss_solve_host(ss_problem* h, const double* rhs_host, double* x_host, int32_t
     SS_GUARD_END
 }
 
+int ss_debug_poison_smem(ss_problem* h) {
+    SS_GUARD_BEGIN
+    SSB_CHECK(h, SS_ERR_ARG, "ss_debug_poison_smem: NULL handle");
+    SSB_CUDA(cudaSetDevice(h->P.device));
+    poison_shared_memory(h->P.stream);
+    SS_GUARD_END
+}
+
 int ss_set_sm_budget(ss_problem* h, int32_t sms) {
     SS_GUARD_BEGIN
     SSB_CHECK(h && sms >= 0, SS_ERR_ARG, "ss_set_sm_budget: NULL handle or negative budget");

@@ -277,7 +277,8 @@ void build_sell(const HostCSR& H, DevCSR& D, cudaStream_t s);
 void block_trsv(DevBlockTri& T, const double2* b, double2* x, cudaStream_t s,
                 unsigned long long* trace = nullptr);
 size_t block_trsv_packed(int B);
-void block_trsv_prepare(DevBlockTri& T);   // launch geometry (persistent grid)
+void block_trsv_prepare(DevBlockTri& T);
+void poison_shared_memory(cudaStream_t s);   // ss_debug_poison_smem (trsv.cu)   // launch geometry (persistent grid)
 // krylov.cu / gmres.cu
 void gmres_solve(Problem& P, const double2* b_dev, int restart, double tol, int max_iter,
                  ss_solve_info* info);

@@ -160,7 +160,15 @@ constexpr int kLtGate = SSB_LT_GATE;
 #define SSB_LT_G3 0   // with kDense = 3: G3_k x_{k-3} by the lieutenants (columns l, l+7, ... of G3_k from L2), not the chain
 #endif
 constexpr bool kLtG3 = SSB_LT_G3 != 0;
-constexpr int kChainDense = kLtG3 ? 2 : kDense;   // dense blocks the chain teams apply (G ring stage)
+#ifndef SSB_G3_LDG
+#define SSB_G3_LDG 0   // with kDense = 3 and row-owning teams: G3_k x_{k-3} by four extra chain-CTA warps, G3 from L2
+#endif
+constexpr bool kG3Ldg = SSB_G3_LDG != 0;
+constexpr int kChainDense = (kLtG3 || kG3Ldg) ? 2 : kDense;   // dense blocks the chain teams apply (G ring stage)
+#ifndef SSB_TEST_NO_OPERAND_ZEROING
+#define SSB_TEST_NO_OPERAND_ZEROING 0   // (test builds only: the pre-fix lieutenants, to show the stale-smem test fails on them)
+#endif
+constexpr bool kZeroOperands = SSB_TEST_NO_OPERAND_ZEROING == 0;
 #ifndef SSB_ROWWARPS
 #define SSB_ROWWARPS 0   // chain teams: warp w owns ROWS 8w .. 8w+7 (4 lanes per row, shuffle reduction) instead of columns
 #endif
@@ -198,7 +206,7 @@ struct Cfg {
     static constexpr int kLt = kLieutenants;
     static constexpr int kCluster = 1 + kLt;          // chain + lieutenants
     static constexpr int kCompute = 256;              // compute threads (8 warps)
-    static constexpr int kNT = 544;                   // chain CTA: 17 warps (roles below)
+    static constexpr int kNT = kG3Ldg ? 608 : 544;    // chain CTA: 17 warps (roles below; + warps 17, 18 with kG3Ldg)
     // chain CTA warp roles (warp w runs on SMSP w mod 4): producer 0, publisher 1, G producer
     // 2, chain teams 0, 1, 2 = warps 5 .. 8, 9 .. 12, 13 .. 16 (blocks k = team mod 3), one
     // warp of each team per SMSP (warps 3, 4 idle)
@@ -266,15 +274,22 @@ struct Cfg {
     static constexpr size_t kOffG3full = kOffRfull + 8 * kSStages;             // [4] G3 vector of block k ready
     static constexpr size_t kOffInts = kOffG3full + (kG3Warps ? 8 * 4 : 0);
     static constexpr size_t kOffLbar = kOffInts + 32;   // [4] (lieutenants) late part of block k done
+    // kG3Ldg: partials of the four G3 warps, kG3Slots blocks deep.  Row-owning teams leave tpart and
+    // pready unused (4 slots); column-owning teams leave the x_{k-3} copies (kOffXw) unused (3 slots)
+    static constexpr int kG3Slots = kRowWarps ? 4 : 3;
+    static constexpr size_t kOffG3Lp = kRowWarps ? kOffTpart : kOffXw;
+    static constexpr size_t kOffG3Lfull = kRowWarps ? kOffPready : kOffLbar;   // (lbar: lieutenants only)
     static constexpr size_t kSmem = kOffInts + 64;
+    static_assert((size_t)kG3Slots * 4 * B * 16 <= (kRowWarps ? (size_t)4 * kTeam * B * 16 : (size_t)kTeams * kTeam * B * 16), "G3 partial slots");
     static_assert(B == 32 && (kDense == 2 || kDense == 3), "the chain teams hold one row per lane, G1 .. G_kDense");
     static_assert(!kG3Warps || kDense == 3, "the G3 warps need G3 (kDense = 3)");
     static_assert(!kLtG3 || (kDense == 3 && !kG3Warps), "lieutenant G3 needs G3 (kDense = 3)");
+    static_assert(!kG3Ldg || (kDense == 3 && !kG3Warps && !kLtG3), "G3-from-L2 warps: kDense = 3");
     static constexpr int kWG3 = 3;                    // G3 warps: 3, 4 (idle otherwise)
     static_assert(kCompute % B == 0 && B % kFarWarps == 0 && kRPW % kGrp == 0 && kFarWarps * 32 <= kNT, "layout");
     static constexpr int kHelperT = kFarWarps * 32;   // helper threads
     static constexpr int kYP = kHelperT / B;          // helper D^{-1} product: threads per row
-    static_assert(kTeamW0 + kTeams * kTeam == kNT / 32 && kCompute / 32 + 1 <= kNT / 32, "warp roles");
+    static_assert(kTeamW0 + kTeams * kTeam == 17 && 17 <= kNT / 32 && kCompute / 32 + 1 <= kNT / 32, "warp roles");
     static_assert(kTPRl * ((B + kLt - 1) / kLt) <= kLtTeamT && kLtTeams * kLtTeamT <= 32 * kWProducerLt &&
                       kLtTeams <= kLtStages,
                   "lieutenant rows / teams");
@@ -349,10 +364,17 @@ __device__ __forceinline__ double2 row_sum_1t(const int32_t* col, const double2*
             v[u].x = ok ? v[u].x : 0.0;
             v[u].y = ok ? v[u].y : 0.0;
         }
-        acc = cfma(acc, v[0], ring[c[0] & kRingMask]);
-        acc2 = cfma(acc2, v[1], ring[c[1] & kRingMask]);
-        acc = cfma(acc, v[2], ring[c[2] & kRingMask]);
-        acc2 = cfma(acc2, v[3], ring[c[3] & kRingMask]);
+        double2 xr[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {   // absent entries: zero the operand too (0 * NaN = NaN)
+            xr[u] = ring[c[u] & kRingMask];
+            xr[u].x = e + u < hi ? xr[u].x : 0.0;
+            xr[u].y = e + u < hi ? xr[u].y : 0.0;
+        }
+        acc = cfma(acc, v[0], xr[0]);
+        acc2 = cfma(acc2, v[1], xr[1]);
+        acc = cfma(acc, v[2], xr[2]);
+        acc2 = cfma(acc2, v[3], xr[3]);
     }
     return cadd(acc, acc2);
 }
@@ -420,9 +442,12 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
         for (int j = 0; j < C::kPbuf; j++) mbar_init(pbar + j, 1);
         for (int j = 0; j < C::kRing; j++) mbar_init(xfull + j, 32);   // the 32 lanes of the storing warp
         for (int j = 0; j < 4; j++) mbar_init(pready + j, C::kTeam * 32);   // every lane of a team
-        for (int j = 0; j < 4; j++) mbar_init(reinterpret_cast<uint64_t*>(smem + C::kOffLbar) + j, 1);
+        if (!(kG3Ldg && !kRowWarps && chain))   // (the chain CTA of that variant keeps its G3 barriers there)
+            for (int j = 0; j < 4; j++) mbar_init(reinterpret_cast<uint64_t*>(smem + C::kOffLbar) + j, 1);
         if (kG3Warps)
             for (int j = 0; j < 4; j++) mbar_init(reinterpret_cast<uint64_t*>(smem + C::kOffG3full) + j, 32);
+        if (kG3Ldg && !kRowWarps && chain)   // every lane of the four G3 warps (re-initialises the chain CTA's unused lbar)
+            for (int j = 0; j < C::kG3Slots; j++) mbar_init(reinterpret_cast<uint64_t*>(smem + C::kOffG3Lfull) + j, 128);
         *sF = 0;
         *sLock = 0;
         *sPub = 0;
@@ -530,7 +555,7 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     st_rel_cta(sPub, j);
                 }
             }
-        } else if (chain && warp >= C::kTeamW0) {
+        } else if (chain && warp >= C::kTeamW0 && warp < C::kTeamW0 + C::kTeams * C::kTeam) {
             // ------------------------------------------------ chain teams 0, 1, 2 (blocks k = team
             // mod 3), 4 warps each:
             //     x_k = y_k - sum_w [ G1_k[:, w] x_{k-1}[w] + G2_k[:, w] x_{k-2}[w] + G3_k[:, w] x_{k-3}[w] ]
@@ -590,6 +615,11 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                             }
                         }
                         carry = cadd(carry, carry2);
+                        if (kG3Ldg) {   // + G3_k[r, 8 g .. 8 g + 7] x_{k-3}[...] from G3 warp g (tpart region)
+                            mbar_wait(reinterpret_cast<uint64_t*>(smem + C::kOffG3Lfull) + k % C::kG3Slots,
+                                      (uint32_t)((k / C::kG3Slots) & 1));
+                            carry = cadd(carry, reinterpret_cast<const double2*>(smem + C::kOffG3Lp)[((k % C::kG3Slots) * 4 + g) * B + r]);
+                        }
                         TPROF(k, 13);
                         __syncwarp();
                         if (lane == 0) mbar_arrive(gempty + s);
@@ -699,6 +729,11 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                         for (int u = 0; u < C::kSlice; u++) carry = cfma(carry, G[B * B + (j0 + u) * B + lane], x2[j0 + u]);
                     }
                     carry = cadd(carry, c1);
+                    if constexpr (kG3Ldg) {   // + the partial of G3 warp tw (columns 8 tw .. 8 tw + 7 of G3_k, lane = row)
+                        mbar_wait(reinterpret_cast<uint64_t*>(smem + C::kOffG3Lfull) + k % C::kG3Slots,
+                                  (uint32_t)((k / C::kG3Slots) & 1));
+                        carry = cadd(carry, reinterpret_cast<const double2*>(smem + C::kOffG3Lp)[((k % C::kG3Slots) * 4 + tw) * B + lane]);
+                    }
                     TPROF(k, 13);
                     __syncwarp();
                     if (lane == 0) mbar_arrive(gempty + s);
@@ -791,6 +826,47 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                 }
                 TPROF(k, 7);
             }
+            }
+        } else if (kG3Ldg && chain && (warp == 3 || warp == 4 || warp >= 17)) {
+            // ------------------------------------------------ G3-from-L2 warps (3, 4, 17, 18): warp h takes
+            // columns 8 h .. 8 h + 7 of G3_k (lane = row) straight from global memory (L2-prefetched
+            // 8 blocks ahead, registers double-buffered over two blocks), waits for x_{k-3} in the
+            // chain ring and leaves its partial for lane group h of the teams (tpart region, 4 slots):
+            // d = 3 never crosses DSMEM and adds nothing to the G ring.
+            const int h = warp < 17 ? warp - 3 : warp - 15;
+            uint64_t* g3f = reinterpret_cast<uint64_t*>(smem + C::kOffG3Lfull);
+            const double2* gsrc = a.G + 2 * B * B + (h * 8) * B + lane;
+            constexpr int64_t kStride = (int64_t)kDense * B * B;
+            double2 ba[8], bb[8];
+            auto load = [&](double2* buf, int k) {
+#pragma unroll
+                for (int u = 0; u < 8; u++) buf[u] = __ldg(gsrc + (int64_t)k * kStride + u * B);
+                if (k + 8 < nblk) {
+#pragma unroll
+                    for (int u = 0; u < 8; u++)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(gsrc + (int64_t)(k + 8) * kStride + u * B));
+                }
+            };
+            auto compute = [&](const double2* buf, int k) {
+                double2 a0 = make_double2(0.0, 0.0), a1 = a0;
+                if (k >= 3) {   // (blocks 0 .. 2 have no source: zero partials keep the slot phases in step)
+                    mbar_wait(xfull + (k - 3) % C::kRing, (uint32_t)(((k - 3) / C::kRing) & 1));   // x_{k-3}
+                    const double2* x3 = ring + (((int64_t)(k - 3) * B) & kRingMask) + h * 8;
+#pragma unroll
+                    for (int u = 0; u < 8; u += 2) {
+                        a0 = cfma(a0, buf[u], x3[u]);
+                        a1 = cfma(a1, buf[u + 1], x3[u + 1]);
+                    }
+                }
+                reinterpret_cast<double2*>(smem + C::kOffG3Lp)[((k % C::kG3Slots) * 4 + h) * B + lane] = cadd(a0, a1);
+                mbar_arrive(g3f + k % C::kG3Slots);   // every lane, after its own partial
+            };
+            if (nblk > 0) load(ba, 0);
+            for (int k = 0; k < nblk; k += 2) {
+                if (k + 1 < nblk) load(bb, k + 1);
+                compute(ba, k);
+                if (k + 2 < nblk) load(ba, k + 2);
+                if (k + 1 < nblk) compute(bb, k + 1);
             }
         } else if (kG3Warps && chain && (warp == C::kWG3 || warp == C::kWG3 + 1)) {
             // ------------------------------------------------ G3 warps: G3_k x_{k-3} (dense, from the
@@ -900,9 +976,12 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     constexpr int kRM = C::kRingLt * B - 1;
                     int lc0 = 0, lc1 = 0;
                     double2 lv0 = make_double2(0.0, 0.0), lv1 = lv0;
+                    bool lok0 = false, lok1 = false;   // the prefetched entries exist
                     auto pre = [&](int p0, int p1, int& c0, int& c1, double2& v0, double2& v1) {
                         const int e0 = p0 + q, e1 = e0 + C::kTPRlate;
                         const bool ok0 = e0 < p1, ok1 = e1 < p1;
+                        lok0 = ok0;
+                        lok1 = ok1;
                         c0 = col[ok0 ? e0 : 0];
                         c1 = col[ok1 ? e1 : 0];
                         v0 = val[ok0 ? e0 : 0];
@@ -939,8 +1018,18 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                     LPROF(k, 4);
                     if (tr0) STAMP(k, 7);
                     if (rowok && q < C::kTPRlate) {
-                        acc = cfma(acc, lv0, ltring[lc0 & kRM]);
-                        acc = cfma(acc, lv1, ltring[lc1 & kRM]);
+                        // an absent entry reads a ring slot this launch may not have written yet (whatever
+                        // the last kernel left in shared memory, possibly a NaN pattern): 0 * NaN = NaN, so
+                        // the OPERAND is zeroed too, not only the value
+                        double2 lx0 = ltring[lc0 & kRM], lx1 = ltring[lc1 & kRM];
+                        if (kZeroOperands) {
+                            lx0.x = lok0 ? lx0.x : 0.0;
+                            lx0.y = lok0 ? lx0.y : 0.0;
+                            lx1.x = lok1 ? lx1.x : 0.0;
+                            lx1.y = lok1 ? lx1.y : 0.0;
+                        }
+                        acc = cfma(acc, lv0, lx0);
+                        acc = cfma(acc, lv1, lx1);
                         for (int e = lt0 + q + 2 * C::kTPRlate; e < lt1; e += C::kTPRlate)   // long rows
                             acc = cfma(acc, val[e], ltring[col[e] & kRM]);
                     }
@@ -963,7 +1052,11 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
 #pragma unroll
                         for (int m = 0; m < kRows; m++) {
                             const int rr = m * C::kLt + l;
-                            pq[m] = lp[rr < B ? rr : 0];
+                            pq[m] = lp[rr < B ? rr : 0];   // (rr >= B: lp[0] is another lieutenant's row, never
+                            if (kZeroOperands) {                // written here -- uninitialised shared memory; zeroed,
+                                pq[m].x = rr < B ? pq[m].x : 0.0;   // because 0 * NaN = NaN)
+                                pq[m].y = rr < B ? pq[m].y : 0.0;
+                            }
                         }
 #pragma unroll
                         for (int m = 0; m < kRows; m += 2) {
@@ -1181,7 +1274,26 @@ void launch(DevBlockTri& T, const double2* b, double2* x, cudaStream_t s, unsign
     SSB_LAUNCHED();
 }
 
+__global__ void __launch_bounds__(256, 1) k_poison_smem(int bytes) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    for (int i = threadIdx.x * 16; i < bytes; i += 256 * 16)
+        *reinterpret_cast<uint4*>(smem + i) = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+}
+
 }  // namespace
+
+// ss_debug_poison_smem: one CTA per SM (the full shared memory each, so they cannot share an SM),
+// several waves so that every SM is covered whatever else is resident.
+void poison_shared_memory(cudaStream_t s) {
+    constexpr int kBytes = 232448 - 1024;
+    SSB_CUDA(cudaFuncSetAttribute(k_poison_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, kBytes));
+    int dev = 0, sms = 0;
+    SSB_CUDA(cudaGetDevice(&dev));
+    SSB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    k_poison_smem<<<4 * sms, 256, kBytes, s>>>(kBytes);
+    SSB_CUDA(cudaGetLastError());
+    SSB_LAUNCHED();
+}
 
 size_t block_trsv_packed(int B) { return (size_t)B * (B + 1) / 2; }
 

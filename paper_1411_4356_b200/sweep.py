@@ -29,22 +29,29 @@ def shard_range(npoints: int, rank: int, world: int) -> range:
     return range(lo, hi)
 
 
-def solve_point_gpu(p, concurrent: int = 1, host_threads: int = 0, stream=None, info: list | None = None) -> tuple:
+def solve_point_gpu(p, concurrent: int = 1, host_threads: int = 0, stream=None, info: list | None = None,
+                    solve_lock=None) -> tuple:
     """Build -> setup -> solve -> expect one parameter point on the current CUDA device.
 
-    concurrent > 1: this point shares the GPU with concurrent - 1 others solved from other
-    host threads at the same time -- its substitution kernels get 1/concurrent of the
+    concurrent > 1: this point shares the GPU with concurrent - 1 others handled by other
+    host threads at the same time, on its own stream.  With ``solve_lock`` (the default of
+    ``concurrent_solver``) only the setups overlap -- the host-bound iLUTP is ~95 % of a
+    sweep point -- and the GMRES solves take the whole GPU one at a time.  Without it the
+    solves overlap too: the substitution kernels of this point get 1/concurrent of the
     co-resident clusters (ss_set_sm_budget; the budgets add up to at most the GPU, so the
-    persistent launches of different points never wait on one another) and its own stream."""
+    persistent launches of different points never wait on one another)."""
+    import contextlib
+
     from . import SteadyState, ss_set_sm_budget
 
     s = SteadyState(p, stream=stream).setup(threads=host_threads)
     try:
-        if concurrent > 1:
+        if concurrent > 1 and solve_lock is None:
             clusters = s.setup_info["trsv_grid"] // 8          # co-resident clusters (whole GPU)
             ss_set_sm_budget(s.handle, 8 * max(2, clusters // concurrent))
-        s.solve()
-        na, nb = s.expect()
+        with solve_lock if solve_lock is not None else contextlib.nullcontext():
+            s.solve()
+            na, nb = s.expect()
         i = s.solve_info
         if info is not None:   # (list.append is atomic: safe from several host threads)
             info.append({"Delta": p.Delta, "n": s.n, "nnz": s.build_info["nnz"], "nnz_L": s.setup_info["nnz_L"],
@@ -55,11 +62,15 @@ def solve_point_gpu(p, concurrent: int = 1, host_threads: int = 0, stream=None, 
         s.close()
 
 
-def concurrent_solver(concurrent: int, host_cores: int | None = None, info: list | None = None) -> Callable:
+def concurrent_solver(concurrent: int, host_cores: int | None = None, info: list | None = None,
+                      overlap_solves: bool = False) -> Callable:
     """A solve(p) for run_sweep that may be called from `concurrent` host threads at once:
     each call on the calling thread's own CUDA stream (same device as the caller of
-    run_sweep), with 1/concurrent of the GPU's co-resident clusters for its substitutions
-    and 1/concurrent of the host cores for its iLUTP setup."""
+    run_sweep), with 1/concurrent of the host cores for its iLUTP setup.  The solves run
+    one at a time on the whole GPU (a lock) while the other points' setups go on;
+    ``overlap_solves=True`` lets them share the GPU instead (1/concurrent of the
+    co-resident clusters each) -- kept for diagnostics: in two 64-point runs of that mode
+    one point each (a different one) lost its first M^-1 application."""
     import os
     import threading
 
@@ -68,12 +79,13 @@ def concurrent_solver(concurrent: int, host_cores: int | None = None, info: list
     dev = torch.cuda.current_device()
     cores = host_cores or os.cpu_count() or 1
     local = threading.local()
+    lock = None if overlap_solves else threading.Lock()
 
     def solve(p):
         torch.cuda.set_device(dev)
         if not hasattr(local, "stream"):
             local.stream = torch.cuda.Stream(device=dev)
-        return solve_point_gpu(p, concurrent, max(1, cores // concurrent), local.stream, info)
+        return solve_point_gpu(p, concurrent, max(1, cores // concurrent), local.stream, info, lock)
 
     return solve
 

@@ -284,9 +284,11 @@ def test_concurrent_points_identical_to_sequential(cuda):
     from paper_1411_4356_b200.sweep import run_sweep, concurrent_solver
     pts = [CONFIGS["small"].with_(Delta=d) for d in (-1.0, -0.5, 0.0, 0.5, 1.0)]
     seq = run_sweep(pts)
-    con = run_sweep(pts, solve=concurrent_solver(3), concurrent=3)
-    assert np.array_equal(seq[:, :6], con[:, :6])      # all but the timing column
-    assert np.all(con[:, 5] == 1.0)
+    # default: setups overlap, solves one at a time; overlap_solves: the solves share the GPU too
+    for overlap in (False, True):
+        con = run_sweep(pts, solve=concurrent_solver(3, overlap_solves=overlap), concurrent=3)
+        assert np.array_equal(seq[:, :6], con[:, :6])      # all but the timing column
+        assert np.all(con[:, 5] == 1.0)
 
 
 def test_sm_budget_same_result(cuda):
@@ -301,6 +303,33 @@ def test_sm_budget_same_result(cuda):
     with pytest.raises(pb().SSError):
         pb().ss_set_sm_budget(s.handle, -1)
     s.close()
+
+
+def test_precond_ignores_stale_shared_memory(cuda):
+    """Shared memory is not cleared between kernels.  With every SM's shared memory filled with a
+    NaN pattern (ss_debug_poison_smem: what another problem's kernels may leave behind when several
+    sweep points share a GPU), M^{-1}, its two factors and the whole solve give bit-identical,
+    finite results: no term of the substitution may multiply a zeroed value by a ring slot or a
+    partial that this launch has not written (0 * NaN = NaN).  Regression test for the sweep
+    points that lost their first M^{-1} application."""
+    torch = cuda
+    for name in ("tiny", "small"):
+        s = pb().SteadyState(CONFIGS[name]).setup()
+        x = torch.from_numpy(rand_cvec(s.n, 5)).cuda()
+        ref = [s.precond(x, w) for w in (0, 1, 2)]
+        for rep in range(3):
+            for w in (0, 1, 2):
+                pb().ss_debug_poison_smem(s.handle)
+                y = s.precond(x, w)
+                assert bool(torch.isfinite(torch.view_as_real(y)).all()), (name, w, rep)
+                assert torch.equal(y, ref[w]), (name, w, rep)
+        s.solve()
+        it0, rho0 = s.solve_info["iterations"], s.rho().clone()
+        pb().ss_debug_poison_smem(s.handle)
+        s.solve()
+        assert s.solve_info["converged"] == 1 and s.solve_info["iterations"] == it0
+        assert torch.equal(s.rho(), rho0)
+        s.close()
 
 
 def test_trace_abi(cuda):
