@@ -941,8 +941,8 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
                         }
                     }
                     double2 g3[kRows];   // (kLtG3) G3_k[tt, l + kLt m]: prefetched into L2 now, loaded below
-                    if (kLtG3 && tt < B && k >= 3) {
-                        const double2* gG3 = a.G + ((int64_t)k * kDense + 2) * B * B + tt;
+                    if (kLtG3 && tt < B && k + C::kLtTeams < nblk) {   // this team's next block: four steps ahead
+                        const double2* gG3 = a.G + ((int64_t)(k + C::kLtTeams) * kDense + 2) * B * B + tt;
 #pragma unroll
                         for (int m = 0; m < kRows; m++) {
                             const int c = m * C::kLt + l;
@@ -1115,7 +1115,10 @@ k_chain_trsv(const TriArgs a, const double2* __restrict__ bvec, double2* out, do
     // per-warp row partial (lane 0, item order: deterministic).  A block's long rows are so
     // spread over all 16 warps, and the items gated by the newest x blocks come last.
     if (warp >= C::kFarWarps) return;
-    constexpr int kHU = 4;
+#ifndef SSB_HU
+#define SSB_HU 4   // far work items in flight per helper warp
+#endif
+    constexpr int kHU = SSB_HU;
     const int H = gridDim.x - C::kCluster;
     int64_t* sRowP = reinterpret_cast<int64_t*>(smem + C::kOffRowP);
     int32_t* sRowL = reinterpret_cast<int32_t*>(smem + C::kOffRowL);
