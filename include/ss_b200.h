@@ -199,8 +199,8 @@ int ss_precond(ss_problem* h, int32_t which, const void* x_dev, void* y_dev);
  * 7 lieutenant 0: x_{k-3} landed, 8 chain team: x_k pushed to the lieutenants,
  * 9 lieutenant 0: q_k sent, 10 chain team: off-chain work of block k done, 11 lieutenant
  * 0: early part done, 12 lieutenant 0: stage of block k ready, 13 chain team: x_{k-1}
- * read; 1, 14, 15 zero.  *nblk_out receives the number of blocks (host_trace may be NULL
- * to query it). */
+ * read; 1, 14, 15 zero (14: only in -DSSB_LT_G3 experiment builds, lieutenant 0 saw
+ * x_{k-3}).  *nblk_out receives the number of blocks (host_trace may be NULL to query it). */
 #define SS_TRACE_STAMPS 16
 int ss_debug_trace_trsv(ss_problem* h, int32_t which, const void* x_dev, void* y_dev, uint64_t* host_trace,
                         int64_t* nblk_out);
